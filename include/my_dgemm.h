@@ -1,0 +1,117 @@
+/*
+ * my_dgemm.h -- C ABI of the B200-native (sm_100a) FP64 GEMM.
+ *
+ * Drop-in for the reference's `my_dgemm` path: C := A*B + C on column-major
+ * float64 matrices with explicit leading dimensions.  Element (i, j) of a
+ * matrix with leading dimension ld is at offset j*ld + i
+ * (reference PAPER.md:273, pkg/src/gemmforge/matrix.py:34-36).
+ *
+ * Every entry point below replaces a reference interface; the citation is on
+ * each declaration (paths relative to /root/reference).  Plain pointers and
+ * sizes only; no torch or CUDA types appear in the signatures (streams are
+ * passed as void*, a cudaStream_t).
+ *
+ * Status codes (int-returning calls):
+ *      0                    success
+ *     -1 .. -9              argument i (1-based: m, n, k, A, lda, B, ldb, C, ldc)
+ *                           is invalid; nothing was read or written.  This is
+ *                           the ValueError of pkg/src/gemmforge/kernels.py:41-49
+ *                           and matrix.py:50-53 (dims < 1, ld < rows, NULL).
+ *    -10                    flags invalid
+ *    -11                    argument out of range for a non-GEMM entry point
+ *     1000 + cudaError_t    CUDA runtime failure (C may be partially written)
+ *     2000 + ncclResult_t   reserved for the collective layer
+ * my_dgemm_last_error() returns a message for the last non-zero status on the
+ * calling thread, in the reference's ValueError wording where one exists.
+ */
+#ifndef MY_DGEMM_B200_H
+#define MY_DGEMM_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MY_DGEMM_API __attribute__((visibility("default")))
+#else
+#define MY_DGEMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Flags for my_dgemm_ex. */
+#define MY_DGEMM_DEVICE_PTRS 0x1u /* A, B, C are device pointers; async on `stream` */
+#define MY_DGEMM_EXACT 0x2u       /* bitwise twin of the reference oracle (verification) */
+#define MY_DGEMM_FORCE_TILED 0x4u /* bypass the m==1 / n==1 bandwidth kernels */
+#define MY_DGEMM_FORCE_VEC1 0x8u  /* force 8-byte operand staging (odd-ld path) */
+
+/*
+ * The BASELINE.json north_star signature.  Replaces the reference's
+ * `my_dgemm(m, n, k, A, lda, B, ldb, C, ldc)` whose
+ * Python realisation is gemm_goto / gemm_goto_parallel
+ * (pkg/src/gemmforge/goto.py:187-239, parallel.py:108-243).  Host pointers,
+ * synchronous.  On invalid arguments C is untouched and the status is kept
+ * for my_dgemm_last_error() / my_dgemm_last_status().
+ */
+MY_DGEMM_API void my_dgemm(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc);
+
+/* Same-signature alias named after the paper's test driver. */
+MY_DGEMM_API void bl_dgemm(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc);
+
+/*
+ * Status-returning form with flags and a CUDA stream (NULL = default stream).
+ * With MY_DGEMM_DEVICE_PTRS the call is asynchronous on `stream`; otherwise
+ * it stages through device memory and returns when C is written back.
+ * Replaces the engine call of the registry variant factory
+ * (pkg/src/gemmforge/registry.py:185-198, `_goto_factory.run`).
+ */
+MY_DGEMM_API int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc,
+                unsigned flags, void *stream);
+
+/*
+ * jc-sharded piece of a multi-GPU GEMM: the caller's rank computes
+ * C[:, j0:j0+nloc] += A[:, p0:p0+kc] * B[p0:p0+kc, j0:j0+nloc] with device
+ * pointers already offset by the caller.  Identical to my_dgemm_ex with
+ * MY_DGEMM_DEVICE_PTRS; kept as a separate symbol so the collective layer's
+ * calls are visible in traces.  Replaces the per-worker block call of
+ * pkg/src/gemmforge/parallel.py:156-164 (`block_call`).
+ */
+MY_DGEMM_API int my_dgemm_shard(int m, int nloc, int kc, const double *A, int lda, const double *B, int ldb, double *C, int ldc,
+                   void *stream);
+
+/*
+ * Device-side splitmix64-v1 operand fill: element (i, j) of the m x n matrix
+ * at `dev` (leading dimension ld) takes stream position t = (col0 + j)*m + i,
+ * i.e. exactly pkg/src/gemmforge/matrix.py:184-207 (`random_values`,
+ * `fill_random`) when col0 = 0.  A non-zero col0 lets a rank fill the column
+ * panel [col0, col0+n) of a larger m x N matrix with the values the full fill
+ * would give it.  Padding rows are never written.  Asynchronous on `stream`.
+ */
+MY_DGEMM_API int my_dgemm_fill_random(double *dev, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0, void *stream);
+
+/* pkg/src/gemmforge/bench.py:89-98 (`_operand_seed`). Pure host integer hash. */
+MY_DGEMM_API uint64_t my_dgemm_operand_seed(uint64_t seed, uint64_t role, int64_t m, int64_t n, int64_t k);
+
+/*
+ * Device-side parity metric (pkg/src/gemmforge/matrix.py:210-232,
+ * `max_abs_diff`): max |X - Y| over the valid m x n region, and the first
+ * element (column-major scan) with |X - Y| > tol, or -1.  Device pointers;
+ * synchronous.  out_first_bad receives the flat index j*m + i.
+ */
+MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
+                          double tol, double *out_max, int64_t *out_first_bad, void *stream);
+
+/* Diagnostics. */
+MY_DGEMM_API const char *my_dgemm_last_error(void);
+MY_DGEMM_API int my_dgemm_last_status(void);
+MY_DGEMM_API const char *my_dgemm_version(void);
+/* Number of kernels this library has launched since load (all threads). */
+MY_DGEMM_API uint64_t my_dgemm_kernel_launches(void);
+/* Release cached device/pinned workspace of the host-pointer path. */
+MY_DGEMM_API void my_dgemm_release_workspace(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MY_DGEMM_B200_H */

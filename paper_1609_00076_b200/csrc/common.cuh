@@ -1,0 +1,49 @@
+// common.cuh -- shared device helpers for the sm_100a FP64 GEMM kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MYD_DEVICE __device__ __forceinline__
+
+namespace myd {
+
+// 64-bit flat index of (i, j) under leading dimension ld (matrix.py:34-36).
+MYD_DEVICE int64_t at(int64_t i, int64_t j, int64_t ld) { return j * ld + i; }
+
+// cp.async (LDGSTS): BYTES in {8, 16}; src_bytes < BYTES zero-fills the tail,
+// src_bytes == 0 reads nothing and writes zeros.
+template <int BYTES>
+MYD_DEVICE void cp_async(void *smem_dst, const void *gmem_src, int src_bytes) {
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem_src), "r"(src_bytes)
+                 : "memory");
+  } else {
+    static_assert(BYTES == 8, "cp.async size");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(gmem_src), "r"(src_bytes)
+                 : "memory");
+  }
+}
+
+MYD_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+template <int N>
+MYD_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// One DMMA.8x8x4: d(8x8) += a(8x4, row) * b(4x8, col).
+// Fragment ownership (lane = threadIdx.x % 32):
+//   a: A[lane/4][lane%4]     b: B[lane%4][lane/4]
+//   c: C[lane/4][2*(lane%4) + {0,1}]
+MYD_DEVICE void dmma_884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Kernel launch counter shared by every launcher (my_dgemm_kernel_launches).
+void count_launch(int n = 1);
+
+}  // namespace myd

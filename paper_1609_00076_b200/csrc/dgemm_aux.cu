@@ -1,0 +1,289 @@
+// dgemm_aux.cu -- the other kernels on the my_dgemm path (sm_100a):
+//   * dgemm_exact   bitwise twin of the reference oracle (verification mode)
+//   * gemv_n1       n == 1   (cfg 3c)  HBM-bound, deterministic in-CTA split-K
+//   * gemv_m1       m == 1   (cfg 3b)  HBM-bound, one warp per column
+//   * fill_random   splitmix64-v1 operand generator, bit-exact with the reference
+//   * max_abs_diff  device-side parity metric
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace myd {
+
+// ---------------------------------------------------------------------------
+// Exact mode.  Per element: acc = C(i,j); for p = 0..K-1 ascending:
+// acc = round(acc + round(A(i,p) * B(p,j))) -- the operation sequence of the
+// reference oracle (_ckernels.pyx:48-59) and of every order-preserving engine
+// (kernels.py:1-7).  __dmul_rn / __dadd_rn forbid contraction into DFMA, so
+// the result is bitwise equal to the CPU oracle.  Only valid k are iterated
+// (no zero padding), so even the sign of a zero C survives exactly.
+// CTA tile 64x64, 256 threads, 4x4 outputs per thread, BK=16 smem slabs.
+// ---------------------------------------------------------------------------
+namespace exact {
+constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256;
+}
+
+__global__ void __launch_bounds__(exact::THREADS)
+    dgemm_exact_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                       int64_t ldb, double *__restrict__ C, int64_t ldc) {
+  using namespace exact;
+  __shared__ double As[BK][BM];
+  __shared__ double Bs[BN][BK + 1];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int row = m0 + tx + 16 * ii, col = n0 + ty + 16 * jj;
+      acc[ii][jj] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
+    }
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    const int kv = min(BK, K - k0);
+    for (int e = tid; e < BK * BM; e += THREADS) {
+      const int kk = e / BM, mm = e % BM;
+      As[kk][mm] = (kk < kv && m0 + mm < M) ? A[(int64_t)(k0 + kk) * lda + m0 + mm] : 0.0;
+    }
+    for (int e = tid; e < BK * BN; e += THREADS) {
+      const int nn = e / BK, kk = e % BK;
+      Bs[nn][kk] = (kk < kv && n0 + nn < N) ? B[(int64_t)(n0 + nn) * ldb + k0 + kk] : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kv; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) a[ii] = As[kk][tx + 16 * ii];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) b[jj] = Bs[ty + 16 * jj][kk];
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[ii][jj] = __dadd_rn(acc[ii][jj], __dmul_rn(a[ii], b[jj]));
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int row = m0 + tx + 16 * ii, col = n0 + ty + 16 * jj;
+      if (row < M && col < N) C[(int64_t)col * ldc + row] = acc[ii][jj];
+    }
+}
+
+cudaError_t launch_dgemm_exact(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream) {
+  using namespace exact;
+  const unsigned gx = (M + BM - 1) / BM, gy = (N + BN - 1) / BN;
+  if (gy > 65535u) {
+    // Column super-panels keep gridDim.y in range for very wide C.
+    for (int64_t nb = 0; nb < N; nb += 65535LL * BN) {
+      const int nn = (int)std::min<int64_t>(65535LL * BN, N - nb);
+      dgemm_exact_kernel<<<dim3(gx, (nn + BN - 1) / BN), THREADS, 0, stream>>>(M, nn, K, A, lda, B + nb * ldb, ldb,
+                                                                                C + nb * ldc, ldc);
+      count_launch();
+    }
+  } else {
+    dgemm_exact_kernel<<<dim3(gx, gy), THREADS, 0, stream>>>(M, N, K, A, lda, B, ldb, C, ldc);
+    count_launch();
+  }
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// n == 1: C(:,0) += A * b.  A is column-major (rows contiguous), b = B(:,0)
+// contiguous.  A CTA owns 32 rows; its 16 warps take interleaved k-slices
+// (warp w: p = w, w+16, ...), each lane one row, so every warp load is one
+// coalesced 256-byte column segment.  Partial sums meet in shared memory and
+// are added in fixed warp order: deterministic, no workspace, one launch.
+// Algorithmic bytes 8*(mk + k + 2m); HBM-bound (cfg 3c).
+// ---------------------------------------------------------------------------
+namespace gemv {
+constexpr int ROWS = 32, WARPS = 16, UNROLL = 8;
+}
+
+__global__ void __launch_bounds__(gemv::ROWS *gemv::WARPS)
+    gemv_n1_kernel(int M, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ b,
+                   double *__restrict__ C) {
+  using namespace gemv;
+  __shared__ double part[WARPS][ROWS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = blockIdx.x * ROWS + lane;
+  double acc = 0.0;
+  if (row < M) {
+    const double *a = A + row;
+    int p = warp;
+    for (; p + (UNROLL - 1) * WARPS < K; p += UNROLL * WARPS) {
+      double av[UNROLL], bv[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        av[u] = __ldcs(a + (int64_t)(p + u * WARPS) * lda);
+        bv[u] = __ldg(b + p + u * WARPS);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) acc = fma(av[u], bv[u], acc);
+    }
+    for (; p < K; p += WARPS) acc = fma(__ldcs(a + (int64_t)p * lda), __ldg(b + p), acc);
+  }
+  part[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && row < M) {
+    double s = C[row];
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) s += part[w][lane];
+    C[row] = s;
+  }
+}
+
+// m == 1: C(0,j) += sum_p A(0,p) B(p,j).  The A row (stride lda) is staged
+// in shared memory chunk by chunk; each warp owns COLS columns and streams
+// them with coalesced 256-byte loads; a fixed xor-shuffle tree reduces.
+namespace gemv {
+constexpr int M1_WARPS = 8, M1_COLS = 2, M1_CHUNK = 4096;
+}
+
+__global__ void __launch_bounds__(gemv::M1_WARPS * 32)
+    gemv_m1_kernel(int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
+                   double *__restrict__ C, int64_t ldc) {
+  using namespace gemv;
+  __shared__ double arow[M1_CHUNK];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j0 = ((int64_t)blockIdx.x * M1_WARPS + warp) * M1_COLS;
+  double acc[M1_COLS];
+#pragma unroll
+  for (int c = 0; c < M1_COLS; ++c) acc[c] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += M1_CHUNK) {
+    const int kv = min(M1_CHUNK, K - k0);
+    __syncthreads();
+    for (int p = threadIdx.x; p < kv; p += blockDim.x) arow[p] = A[(int64_t)(k0 + p) * lda];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < M1_COLS; ++c) {
+      const int64_t j = j0 + c;
+      if (j >= N) break;
+      const double *bc = B + j * ldb + k0;
+      int p = lane;
+      for (; p + 96 < kv; p += 128) {
+        const double b0 = __ldcs(bc + p), b1 = __ldcs(bc + p + 32), b2 = __ldcs(bc + p + 64), b3 = __ldcs(bc + p + 96);
+        acc[c] = fma(arow[p], b0, acc[c]);
+        acc[c] = fma(arow[p + 32], b1, acc[c]);
+        acc[c] = fma(arow[p + 64], b2, acc[c]);
+        acc[c] = fma(arow[p + 96], b3, acc[c]);
+      }
+      for (; p < kv; p += 32) acc[c] = fma(arow[p], __ldcs(bc + p), acc[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < M1_COLS; ++c) {
+    double v = acc[c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int64_t j = j0 + c;
+    if (lane == 0 && j < N) C[j * ldc] = C[j * ldc] + v;
+  }
+}
+
+cudaError_t launch_gemv_n1(int M, int K, const double *A, int64_t lda, const double *b, double *C,
+                           cudaStream_t stream) {
+  using namespace gemv;
+  gemv_n1_kernel<<<(M + ROWS - 1) / ROWS, ROWS * WARPS, 0, stream>>>(M, K, A, lda, b, C);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                           int64_t ldc, cudaStream_t stream) {
+  using namespace gemv;
+  const int64_t per_cta = (int64_t)M1_WARPS * M1_COLS;
+  const int64_t grid = (N + per_cta - 1) / per_cta;
+  gemv_m1_kernel<<<(unsigned)grid, M1_WARPS * 32, 0, stream>>>(N, K, A, lda, B, ldb, C, ldc);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// splitmix64-v1 fill (matrix.py:172-207): element (i, j) of an m x N matrix
+// takes stream position t = j*m + i; value ((mix64(seed + (t+1)G) >> 11) *
+// 2^-52) - 1, every step exact, so the device values equal the reference's
+// bit for bit.  col0 offsets j for column-panel (per-rank) fills.
+// ---------------------------------------------------------------------------
+MYD_DEVICE uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_random_kernel(double *__restrict__ out, int64_t m, int64_t n, int64_t ld, uint64_t seed,
+                                   int64_t col0) {
+  const int64_t rows_per_cta = (int64_t)blockDim.x * 4;
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const uint64_t tbase = (uint64_t)((col0 + j) * m);
+    for (int64_t i = (int64_t)blockIdx.x * rows_per_cta + threadIdx.x; i < m; i += (int64_t)gridDim.x * rows_per_cta) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t ii = i + (int64_t)u * blockDim.x;
+        if (ii < m) {
+          const uint64_t z = mix64(seed + (tbase + (uint64_t)ii + 1ULL) * 0x9E3779B97F4A7C15ULL);
+          out[j * ld + ii] = __dsub_rn(__dmul_rn((double)(z >> 11), 0x1p-52), 1.0);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
+                               cudaStream_t stream) {
+  const int threads = 256;
+  const int64_t gx = std::min<int64_t>((m + threads * 4 - 1) / (threads * 4), 1024);
+  const int64_t gy = std::min<int64_t>(n, 65535);
+  fill_random_kernel<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, stream>>>(out, m, n, ld, seed, col0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// max_abs_diff (matrix.py:210-232): max |X-Y| over the valid region and the
+// first flat index t = j*m + i with |X-Y| > tol (NaN counts as bad).  Max and
+// min are order-independent, so atomics keep the answer deterministic.
+// Non-negative doubles order like their bit patterns, NaN above +inf.
+// ---------------------------------------------------------------------------
+__global__ void max_abs_diff_kernel(int64_t m, int64_t n, const double *__restrict__ X, int64_t ldx,
+                                    const double *__restrict__ Y, int64_t ldy, double tol,
+                                    unsigned long long *out_max_bits, unsigned long long *out_first) {
+  unsigned long long local_max = 0ULL, local_first = ~0ULL;
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+      const double d = fabs(X[j * ldx + i] - Y[j * ldy + i]);
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+      local_max = bits > local_max ? bits : local_max;
+      if (!(d <= tol)) {
+        const unsigned long long t = (unsigned long long)(j * m + i);
+        local_first = t < local_first ? t : local_first;
+      }
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long om = __shfl_xor_sync(0xffffffffu, local_max, off);
+    const unsigned long long of = __shfl_xor_sync(0xffffffffu, local_first, off);
+    local_max = om > local_max ? om : local_max;
+    local_first = of < local_first ? of : local_first;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out_max_bits, local_max);
+    atomicMin(out_first, local_first);
+  }
+}
+
+cudaError_t launch_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
+                                double tol, unsigned long long *d_out2, cudaStream_t stream) {
+  const int threads = 256;
+  const int64_t gx = std::min<int64_t>((m + threads - 1) / threads, 64);
+  const int64_t gy = std::min<int64_t>(n, 4096);
+  max_abs_diff_kernel<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, stream>>>(m, n, X, ldx, Y, ldy, tol, d_out2,
+                                                                                d_out2 + 1);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace myd

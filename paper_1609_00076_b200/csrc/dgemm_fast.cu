@@ -1,0 +1,190 @@
+// dgemm_fast.cu -- the hot path: C := A*B + C, FP64, column-major, any ld, on sm_100a.
+//
+// The reference's five BLIS loops (pkg/src/gemmforge/goto.py:187-239 and
+// _ckernels.pyx:15-45,142-195) re-derived for Blackwell:
+//   loop 5/3 (jc, ic)  -> the CTA grid over 128x128 tiles of C, rastered in
+//                         bands of GROUP_M tile-rows so co-resident CTAs share
+//                         A and B panels in the 126 MB L2;
+//   loop 4 (pc)        -> the in-CTA K loop over BK=16 slabs;
+//   pack_a / pack_b    -> cp.async (LDGSTS) staging of the A and B slabs into a
+//                         STAGES-deep shared-memory ring; zero-fill of the
+//                         out-of-range lanes replaces the zero-padded panels;
+//                         no separate pack pass touches HBM;
+//   loops 2/1 + _mk    -> 8 warps, each a 64x32 register tile of C built from
+//                         8x4 DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
+//                         no tcgen05 kind on sm_100a; the DMMA pipe measured
+//                         37.1 TFLOP/s (128 flop/clk/SM) vs 34.0 for DFMA
+//                         (tools/microbench/fp64_peak.cu, profiles/).
+// C is loaded into the accumulators first, like _mk's tile load
+// (_ckernels.pyx:28-32), and only the valid region is stored back.
+#include "common.cuh"
+
+namespace myd {
+
+namespace fast {
+constexpr int BM = 128;          // CTA tile rows (m)
+constexpr int BN = 128;          // CTA tile cols (n)
+constexpr int BK = 16;           // K slab per pipeline stage
+constexpr int STAGES = 4;        // cp.async ring depth
+constexpr int THREADS = 256;     // 8 warps: 2 (m) x 4 (n)
+constexpr int WM = 64, WN = 32;  // warp tile
+constexpr int FM = WM / 8, FN = WN / 8;
+// Padded pitches make every fragment load and every 16-byte staging store
+// conflict-free: a half-warp's 4 k-rows of A (4 n-rows of B) land in 4
+// distinct 32-byte bank groups (pitch = 4 mod 16 doubles).
+constexpr int AP = BM + 4;  // A slab: [BK][AP]   (m contiguous, as in HBM)
+constexpr int BP = BK + 4;  // B slab: [BN][BP]   (k contiguous, as in HBM)
+constexpr int A_STAGE = BK * AP;
+constexpr int B_STAGE = BN * BP;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+constexpr int GROUP_M = 8;
+}  // namespace fast
+
+// VEC doubles per cp.async (2: 16-byte copies, needs even ld and 16-B aligned
+// bases; 1: 8-byte copies for odd leading dimensions / 8-B aligned views).
+template <int VEC>
+__global__ void __launch_bounds__(fast::THREADS, 1)
+    dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+  using namespace fast;
+  extern __shared__ __align__(128) double smem[];
+  double *As = smem;
+  double *Bs = smem + STAGES * A_STAGE;
+
+  // Grouped raster: GROUP_M tile-rows per band, column-major inside a band.
+  const int bid = blockIdx.x;
+  const int band = GROUP_M * tiles_n;
+  const int first_m = (bid / band) * GROUP_M;
+  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (bid % band) % gm;
+  const int tn = (bid % band) / gm;
+  const int m0 = tm * BM, n0 = tn * BN;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int r = lane >> 2, q = lane & 3;
+
+  const int KT = (K + BK - 1) / BK;
+
+  // ---- staging (pack_a / pack_b equivalent) ----
+  auto load_stage = [&](int slot, int kt) {
+    const int kbase = kt * BK;
+    double *as = As + slot * A_STAGE;
+    double *bs = Bs + slot * B_STAGE;
+    constexpr int A_COPIES = BK * BM / VEC / THREADS;
+#pragma unroll
+    for (int c = 0; c < A_COPIES; ++c) {
+      const int e = (tid + c * THREADS) * VEC;
+      const int kk = e / BM, mm = e % BM;
+      const int gk = kbase + kk, gmr = m0 + mm;
+      int bytes = 0;
+      const double *src = A;
+      if (gk < K && gmr < M) {
+        bytes = min(VEC, M - gmr) * 8;
+        src = A + (int64_t)gk * lda + gmr;
+      }
+      cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
+    }
+    constexpr int B_COPIES = BK * BN / VEC / THREADS;
+#pragma unroll
+    for (int c = 0; c < B_COPIES; ++c) {
+      const int e = (tid + c * THREADS) * VEC;
+      const int nn = e / BK, kk = e % BK;
+      const int gk = kbase + kk, gn = n0 + nn;
+      int bytes = 0;
+      const double *src = B;
+      if (gn < N && gk < K) {
+        bytes = min(VEC, K - gk) * 8;
+        src = B + (int64_t)gn * ldb + gk;
+      }
+      cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
+    }
+  };
+
+  // ---- prologue: start the ring, then load C into the accumulators ----
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  double acc[FM][FN][2];
+  const int row0 = m0 + wm * WM + r;
+  const int col0 = n0 + wn * WN + 2 * q;
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = row0 + i * 8, col = col0 + j * 8 + e;
+        acc[i][j][e] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
+      }
+
+  // Per-thread fragment offsets inside a stage.
+  const int a_off = q * AP + wm * WM + r;  // + kk*4*AP + i*8
+  const int b_off = (wn * WN + r) * BP + q;  // + j*8*BP + kk*4
+
+  // ---- main loop (loop 4, pc) ----
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_async_commit();
+    }
+    const double *as = As + (kt % STAGES) * A_STAGE + a_off;
+    const double *bs = Bs + (kt % STAGES) * B_STAGE + b_off;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[FM], b[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) a[i] = as[kk * 4 * AP + i * 8];
+#pragma unroll
+      for (int j = 0; j < FN; ++j) b[j] = bs[j * 8 * BP + kk * 4];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- epilogue: valid region only (padding rows never touched) ----
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = row0 + i * 8, col = col0 + j * 8 + e;
+        if (row < M && col < N) C[(int64_t)col * ldc + row] = acc[i][j][e];
+      }
+}
+
+cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1) {
+  using namespace fast;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const long long tiles = (long long)tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const bool aligned16 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  // Set on every call: cheap, per-device, and thread-safe without a flag.
+  if (aligned16 && !force_vec1) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    dgemm_fast_kernel<2><<<(unsigned)tiles, THREADS, SMEM_BYTES, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
+                                                                           tiles_n);
+  } else {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    dgemm_fast_kernel<1><<<(unsigned)tiles, THREADS, SMEM_BYTES, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
+                                                                           tiles_n);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace myd

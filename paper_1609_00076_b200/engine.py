@@ -1,0 +1,244 @@
+"""Host-side mirror of the reference's engine / plugin interface for the
+my_dgemm path, over the sm_100a C ABI.
+
+The reference (Python package `gemmforge`, /root/reference/pkg) selects GEMM
+engines by name through `KernelRegistry.register_variant(name, factory)`
+(pkg/src/gemmforge/registry.py:113-125); a factory maps a config to
+`engine(a, b, c, backend=None, stats=None, **kw) -> c` (the shape of
+`_goto_factory`, registry.py:185-198) over column-major `Matrix` objects
+(matrix.py:39-87).  This module provides exactly that surface:
+
+  * `Matrix`, `check_conformal`  -- same attributes, same ValueError wording;
+  * `gemm_b200(a, b, c)`         -- the engine (the drop-in for gemm_goto /
+                                    gemm_goto_parallel, goto.py:187,
+                                    parallel.py:108);
+  * `b200_factory(cfg)`          -- the registry factory;
+  * `register(registry)`         -- `registry.register_variant("b200", ...)`,
+                                    which runs the reference's own validation
+                                    gate (registry.py:127-137) when given the
+                                    reference registry;
+  * `my_dgemm(...)`              -- the flat-buffer BASELINE signature.
+
+Any object with `.m .n .ld .data` (a float64 1-D numpy array) is accepted as a
+matrix, so the reference's own Matrix instances work unchanged.  Device
+operands (torch CUDA tensors as `.data`) run asynchronously on the current
+stream; host operands stage through the library's device workspace.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _capi
+
+__all__ = [
+    "Matrix",
+    "alloc_matrix",
+    "check_conformal",
+    "gemm_b200",
+    "b200_factory",
+    "register",
+    "my_dgemm",
+    "dgemm_device",
+    "fill_random_device",
+    "operand_seed",
+    "max_abs_diff_device",
+    "kernel_launches",
+]
+
+
+class Matrix:
+    """Column-major float64 matrix over an explicit leading dimension.
+
+    Mirrors gemmforge.matrix.Matrix (matrix.py:39-87): element (i, j) at
+    data[j*ld + i]; data must hold at least ld*(n-1)+m elements.
+    """
+
+    __slots__ = ("m", "n", "ld", "data")
+
+    def __init__(self, m: int, n: int, ld: int, data):
+        if m < 1 or n < 1:
+            raise ValueError(f"matrix dims must be positive, got m={m} n={n}")
+        if ld < m:
+            raise ValueError(f"leading dimension ld={ld} smaller than row count m={m}")
+        _check_buffer(data, ld * (n - 1) + m)
+        self.m, self.n, self.ld, self.data = m, n, ld, data
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.m, self.n)
+
+    def __repr__(self) -> str:
+        return f"Matrix(m={self.m}, n={self.n}, ld={self.ld})"
+
+
+def alloc_matrix(m: int, n: int, ld: int | None = None) -> Matrix:
+    """Zeroed host matrix (matrix.py:120-128)."""
+    ld = m if ld is None else ld
+    if m < 1 or n < 1:
+        raise ValueError(f"matrix dims must be positive, got m={m} n={n}")
+    if ld < m:
+        raise ValueError(f"leading dimension ld={ld} smaller than row count m={m}")
+    return Matrix(m, n, ld, np.zeros(ld * n, dtype=np.float64))
+
+
+def _is_device(data) -> bool:
+    return hasattr(data, "__cuda_array_interface__") or (
+        hasattr(data, "is_cuda") and bool(getattr(data, "is_cuda"))
+    )
+
+
+def _check_buffer(data, need: int) -> None:
+    if _is_device(data):
+        import torch
+
+        if data.dtype != torch.float64 or data.dim() != 1 or not data.is_contiguous():
+            raise ValueError("data must be a 1-D float64 ndarray")
+        size = data.numel()
+    else:
+        if not isinstance(data, np.ndarray) or data.dtype != np.float64 or data.ndim != 1:
+            raise ValueError("data must be a 1-D float64 ndarray")
+        if not data.flags.c_contiguous:
+            raise ValueError("data must be contiguous")
+        size = data.size
+    if size < need:
+        raise ValueError(f"buffer too small: need {need} elements, got {size}")
+
+
+def _ptr(data) -> int:
+    if isinstance(data, np.ndarray):
+        return data.ctypes.data
+    return int(data.data_ptr())
+
+
+def check_conformal(a, b, c) -> tuple[int, int, int]:
+    """Validate C(m,n) := A(m,k) * B(k,n) + C (kernels.py:41-49, same messages)."""
+    if a.n != b.m:
+        raise ValueError(f"inner dims differ: A is {a.m}x{a.n}, B is {b.m}x{b.n}")
+    if c.m != a.m or c.n != b.n:
+        raise ValueError(
+            f"C is {c.m}x{c.n}, expected {a.m}x{b.n} from A {a.m}x{a.n} * B {b.m}x{b.n}"
+        )
+    return a.m, b.n, a.n
+
+
+def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False) -> int:
+    f = _capi.EXACT if exact else 0
+    f |= _capi.FORCE_TILED if force_tiled else 0
+    f |= _capi.FORCE_VEC1 if force_vec1 else 0
+    return f
+
+
+def gemm_b200(a, b, c, backend=None, stats=None, exact: bool = False, stream=None, **kw):
+    """C := A*B + C on the B200.  Reference engine signature (registry.py:190).
+
+    `backend` is accepted and ignored (the reference's CPU backend switch,
+    backends.py:93-100, has no meaning for the GPU engine).  `stats`, when a
+    dict, counts launches under "gpu_calls".  exact=True selects the bitwise
+    oracle twin.  Host operands: synchronous.  Device operands (torch CUDA
+    tensors, all three): asynchronous on `stream` (default: torch's current
+    stream).
+    """
+    m, n, k = check_conformal(a, b, c)
+    for mat, rows in ((a, m), (b, k), (c, m)):
+        _check_buffer(mat.data, mat.ld * (mat.n - 1) + rows)
+    dev = [_is_device(x.data) for x in (a, b, c)]
+    lib = _capi.load()
+    flags = _flags(exact, kw.get("force_tiled", False), kw.get("force_vec1", False))
+    if all(dev):
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(c.data.device).cuda_stream
+        st = lib.my_dgemm_ex(m, n, k, _ptr(a.data), a.ld, _ptr(b.data), b.ld, _ptr(c.data), c.ld,
+                             flags | _capi.DEVICE_PTRS, ctypes.c_void_p(stream))
+    elif not any(dev):
+        st = lib.my_dgemm_ex(m, n, k, _ptr(a.data), a.ld, _ptr(b.data), b.ld, _ptr(c.data), c.ld,
+                             flags, None)
+    else:
+        raise ValueError("operands must be all host or all device buffers")
+    _capi.check(st)
+    if stats is not None:
+        stats["gpu_calls"] = stats.get("gpu_calls", 0) + 1
+    return c
+
+
+def b200_factory(cfg=None):
+    """Registry factory (registry.py:185-198 shape).  The CPU blocking
+    parameters in cfg.goto / cfg.threads do not apply to the GPU engine and
+    are ignored; `cfg.exact` (optional) selects the bitwise twin."""
+    exact = bool(getattr(cfg, "exact", False)) if cfg is not None else False
+
+    def run(a, b, c, backend=None, stats=None, **kw):
+        return gemm_b200(a, b, c, backend=backend, stats=stats, exact=kw.pop("exact", exact), **kw)
+
+    return run
+
+
+def register(registry=None, name: str = "b200", validate: bool = True):
+    """Register the engine as a named variant.  With the reference registry
+    (gemmforge.registry.default_registry()) this passes through its own
+    validation gate (registry.py:127-137) before it becomes selectable."""
+    if registry is None:
+        from gemmforge.registry import default_registry  # the reference package
+
+        registry = default_registry()
+    if name in registry.variant_names():
+        return registry.variant(name)
+    return registry.register_variant(name, b200_factory, validate=validate)
+
+
+def my_dgemm(m: int, n: int, k: int, A: np.ndarray, lda: int, B: np.ndarray, ldb: int,
+             C: np.ndarray, ldc: int, exact: bool = False) -> np.ndarray:
+    """The BASELINE signature on flat host buffers.  Checks the
+    buffer lengths the C ABI cannot see, then calls my_dgemm_ex."""
+    if m < 1 or n < 1 or k < 1:
+        raise ValueError(f"matrix dims must be positive, got m={m} n={n} k={k}")
+    Matrix(m, k, lda, A), Matrix(k, n, ldb, B), Matrix(m, n, ldc, C)
+    lib = _capi.load()
+    _capi.check(lib.my_dgemm_ex(m, n, k, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc,
+                                _flags(exact), None))
+    return C
+
+
+def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int, ldc: int,
+                 stream: int = 0, exact: bool = False, force_tiled: bool = False,
+                 force_vec1: bool = False) -> None:
+    """Raw device-pointer call (asynchronous on `stream`)."""
+    lib = _capi.load()
+    _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
+                                _flags(exact, force_tiled, force_vec1) | _capi.DEVICE_PTRS,
+                                ctypes.c_void_p(stream)))
+
+
+def fill_random_device(ptr: int, m: int, n: int, ld: int, seed: int, col0: int = 0,
+                       stream: int = 0) -> None:
+    """splitmix64-v1 fill on the device, bit-exact with fill_random (matrix.py:197-207)."""
+    lib = _capi.load()
+    _capi.check(lib.my_dgemm_fill_random(ptr, m, n, ld, seed & 0xFFFFFFFFFFFFFFFF, col0,
+                                         ctypes.c_void_p(stream)))
+
+
+def operand_seed(seed: int, role: int, m: int, n: int, k: int) -> int:
+    """bench.py:89-98 `_operand_seed`."""
+    return int(_capi.load().my_dgemm_operand_seed(seed & 0xFFFFFFFFFFFFFFFF, role, m, n, k))
+
+
+def max_abs_diff_device(m: int, n: int, x_ptr: int, ldx: int, y_ptr: int, ldy: int,
+                        tol: float = 0.0, stream: int = 0) -> tuple[float, int | None, int | None]:
+    """matrix.py:210-232 on the device: (max |X-Y|, first_bad_i, first_bad_j)."""
+    lib = _capi.load()
+    mx = ctypes.c_double()
+    first = ctypes.c_int64()
+    _capi.check(lib.my_dgemm_max_abs_diff(m, n, x_ptr, ldx, y_ptr, ldy, tol, ctypes.byref(mx),
+                                          ctypes.byref(first), ctypes.c_void_p(stream)))
+    if first.value < 0:
+        return mx.value, None, None
+    j, i = divmod(first.value, m)
+    return mx.value, i, j
+
+
+def kernel_launches() -> int:
+    return int(_capi.load().my_dgemm_kernel_launches())

@@ -1,0 +1,275 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI, against the
+oracle and the reference-generated golden fixtures.
+
+Bars (BASELINE.json north_star):
+  * exact mode (MY_DGEMM_EXACT) and the operand generator: BIT-EXACT;
+  * fast path: |C - C_ref|_max <= c * k * eps * (|A||B| + |C|)_max with
+    c = 2, eps = 2^-52 (HEADLINE_C below), checked elementwise, plus the
+    reference's own gate 2^-50 * k * max|A| * max|B| (kernels.py:31-38).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1609_00076_b200 import _capi, engine
+
+pytestmark = pytest.mark.gpu
+
+HEADLINE_C = 2.0
+EPS = 2.0**-52
+SEED = 42
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _capi.load()
+    return torch
+
+
+def dev_matrix(torch, m, n, ld, seed, canary=None, col0=0):
+    """Device buffer ld*n filled by the device generator (padding = canary)."""
+    buf = torch.full((ld * n,), canary if canary is not None else 0.0, dtype=torch.float64,
+                     device="cuda")
+    engine.fill_random_device(buf.data_ptr(), m, n, ld, seed, col0,
+                              torch.cuda.current_stream().cuda_stream)
+    return buf
+
+
+def dev_operands(torch, m, n, k, lda=None, ldb=None, ldc=None, canary=None):
+    lda, ldb, ldc = lda or m, ldb or k, ldc or m
+    s = [oracle.operand_seed(SEED, r, m, n, k) for r in (1, 2, 3)]
+    return (dev_matrix(torch, m, k, lda, s[0], canary), dev_matrix(torch, k, n, ldb, s[1], canary),
+            dev_matrix(torch, m, n, ldc, s[2], canary), (lda, ldb, ldc))
+
+
+def run_dev(torch, m, n, k, a, lda, b, ldb, c, ldc, **kw):
+    engine.dgemm_device(m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), ldc,
+                        torch.cuda.current_stream().cuda_stream, **kw)
+    torch.cuda.synchronize()
+
+
+def headline_bound(m, n, k, a, lda, b, ldb, c0, ldc):
+    A = oracle.valid_region(a, m, k, lda).T
+    B = oracle.valid_region(b, k, n, ldb).T
+    C = oracle.valid_region(c0, m, n, ldc).T
+    mag = np.abs(A) @ np.abs(B) + np.abs(C)
+    return HEADLINE_C * k * EPS * float(mag.max())
+
+
+# ------------------------------------------------------------------ generator
+
+
+@pytest.mark.parametrize("m,n,ld,seed,col0", [
+    (2, 4, 2, 42, 0), (3, 5, 7, 9, 0), (37, 23, 40, 7, 0), (1000, 3, 1001, (1 << 64) - 1, 0),
+    (129, 17, 129, 12345678901234567, 5), (4093, 7, 4100, 0, 11),
+])
+def test_fill_random_bit_exact(torch_cuda, m, n, ld, seed, col0):
+    canary = -777.25
+    d = dev_matrix(torch_cuda, m, n, ld, seed, canary, col0)
+    got = d.cpu().numpy()
+    want = oracle.random_values(seed, m * (n + col0))[col0 * m:]
+    assert np.array_equal(oracle.valid_region(got, m, n, ld).ravel(), want)
+    if ld > m:
+        assert np.all(got.reshape(n, ld)[:, m:] == canary)
+
+
+def test_fill_matches_reference_goldens(torch_cuda, golden):
+    d = dev_matrix(torch_cuda, 2, 4, 2, 42).cpu().numpy()
+    assert d.tolist() == golden["random_values"]["seed42_first8"]
+
+
+# ------------------------------------------------------------ exact (bitwise)
+
+EXACT_KATS = ["cfg3d", "cfg1", "cfg2_256", "cfg2_768", "cfg2_1024", "cfg3b", "cfg3c", "cfg3a",
+              "cfg2_2048", "cfg4"]
+
+
+@pytest.mark.parametrize("name", EXACT_KATS)
+def test_exact_mode_bitwise_kat(torch_cuda, golden, name):
+    kat = golden["kat"][name]
+    m, n, k = kat["m"], kat["n"], kat["k"]
+    lda, ldb, ldc = kat["lds"]
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc, exact=True)
+    got = c.cpu().numpy()
+    assert oracle.sha256_valid(got, m, n, ldc) == kat["sha256"]
+    if ldc > m:
+        assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
+
+
+def test_exact_mode_host_path_matches_oracle_bitwise(torch_cuda):
+    for (m, n, k) in [(1, 1, 1), (5, 4, 3), (8, 8, 8), (13, 11, 17), (97, 89, 83), (130, 257, 33)]:
+        a, b, c = oracle.make_padded_operands(SEED, m, n, k, m + 2, k + 1, m + 3)
+        want = oracle.naive(m, n, k, a, m + 2, b, k + 1, c.copy(), m + 3)
+        got = engine.my_dgemm(m, n, k, a, m + 2, b, k + 1, c.copy(), m + 3, exact=True)
+        assert np.array_equal(got, want), (m, n, k)
+
+
+# ------------------------------------------------------------ fast path
+
+
+def check_fast_vs_oracle(m, n, k, lda, ldb, ldc, want=None, **kw):
+    a, b, c0 = oracle.make_padded_operands(SEED, m, n, k, lda, ldb, ldc, canary=-777.25)
+    if want is None:
+        want = oracle.naive_par(m, n, k, a, lda, b, ldb, c0.copy(), ldc)
+    got = engine.my_dgemm(m, n, k, a, lda, b, ldb, c0.copy(), ldc)
+    bound = headline_bound(m, n, k, a, lda, b, ldb, c0, ldc)
+    rep = oracle.max_abs_diff(got, want, m, n, ldc, tol=bound)
+    assert rep.clean, oracle.failure_line(rep.first_bad_i, rep.first_bad_j, rep.value_got,
+                                          rep.value_expected)
+    gate = oracle.tolerance(k, 1.0, 1.0)
+    assert rep.max_abs_diff <= gate
+    pad = got.reshape(n, ldc)[:, m:] if ldc > m else np.zeros(0)
+    assert np.all(pad == -777.25), "padding rows of C were written"
+    return rep
+
+
+@pytest.mark.parametrize("m,n,k", [
+    (1, 1, 1), (2, 3, 1), (5, 4, 3), (8, 8, 8), (9, 7, 11), (31, 33, 32), (37, 53, 71),
+    (64, 64, 64), (97, 89, 83), (127, 129, 15), (128, 128, 16), (129, 127, 17), (255, 257, 300),
+    (512, 512, 512),
+])
+@pytest.mark.parametrize("pad", [0, 1, 2, 7])
+def test_fast_small_and_ragged(torch_cuda, m, n, k, pad):
+    check_fast_vs_oracle(m, n, k, m + pad, k + (pad * 5) % 8, m + (pad * 3) % 8)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg3d", "cfg3a", "cfg3b", "cfg3c", "cfg2_1024"])
+def test_fast_baseline_configs(torch_cuda, golden, name):
+    kat = golden["kat"][name]
+    m, n, k = kat["m"], kat["n"], kat["k"]
+    lda, ldb, ldc = kat["lds"]
+    check_fast_vs_oracle(m, n, k, lda, ldb, ldc)
+
+
+def test_fast_vec1_path_matches(torch_cuda):
+    """Odd leading dimensions force 8-byte staging; both staging widths agree bitwise."""
+    m, n, k = 300, 200, 100
+    a, b, c, (lda, ldb, ldc) = dev_operands(torch_cuda, m, n, k, 301, 103, 305)
+    c2 = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c2, ldc, force_vec1=True)
+    assert torch_cuda.equal(c, c2)
+
+
+def test_fast_tiled_handles_skinny(torch_cuda, golden):
+    """The tiled kernel is also correct on m==1 / n==1 (bypass the gemv kernels)."""
+    for name in ("cfg3b", "cfg3c"):
+        kat = golden["kat"][name]
+        m, n, k = kat["m"], kat["n"], kat["k"]
+        lda, ldb, ldc = kat["lds"]
+        a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc)
+        ce = c.clone()
+        run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc, force_tiled=True)
+        run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+        bound = HEADLINE_C * k * EPS * 2.0 * k
+        mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
+        assert i is None and mx <= bound
+
+
+def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
+    """cfg2 at 8192^3: every element of the fast result against the exact
+    (bitwise-oracle) kernel, and the reference's sampled elements."""
+    m = n = k = 8192
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    ce = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, c, m)
+    run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
+    # |A||B|+|C| <= k + 1 for entries in [-1, 1)
+    bound = HEADLINE_C * k * EPS * (k + 1)
+    mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), m, ce.data_ptr(), m, bound)
+    assert i is None, (i, j, mx)
+    s = golden["sampled"]["cfg2_8192"]
+    host_c = c.view(n, m)
+    host_e = ce.view(n, m)
+    for t, (i, j) in enumerate((i, j) for i in s["rows"] for j in s["cols"]):
+        assert float(host_e[j, i]) == s["values"][t]  # exact kernel: bitwise
+        assert abs(float(host_c[j, i]) - s["values"][t]) <= bound
+
+
+def test_fast_deterministic(torch_cuda):
+    m, n, k = 1000, 1100, 1200
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    outs = []
+    for _ in range(3):
+        cc = c.clone()
+        run_dev(torch_cuda, m, n, k, a, m, b, k, cc, m)
+        outs.append(cc)
+    assert torch_cuda.equal(outs[0], outs[1]) and torch_cuda.equal(outs[0], outs[2])
+
+
+def test_kchunked_equals_unchunked_bitwise(torch_cuda):
+    """C += A[:,chunk] B[chunk,:] over 16-aligned k chunks is bitwise the
+    single call (the multi-GPU driver relies on it)."""
+    m, n, k = 640, 384, 1024
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    c1 = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, c1, m)
+    c2 = c.clone()
+    for p0 in range(0, k, 256):
+        engine.dgemm_device(m, n, 256, a.data_ptr() + p0 * m * 8, m, b.data_ptr() + p0 * 8, k,
+                            c2.data_ptr(), m, torch_cuda.cuda.current_stream().cuda_stream)
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(c1, c2)
+
+
+# ------------------------------------------------------------ boundary
+
+
+def test_small_cases_against_reference_fixtures(torch_cuda, small_cases):
+    for key, want in small_cases.items():
+        if not key.startswith("verify_"):
+            continue
+        m, n, k = (int(x) for x in key.split("_")[1:])
+        a, b, c = oracle.make_operands(SEED, m, n, k)
+        got = engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m, exact=True)
+        assert np.array_equal(oracle.valid_region(got, m, n, m).T, want), key
+        got = engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m)
+        assert np.abs(oracle.valid_region(got, m, n, m).T - want).max() <= oracle.tolerance(k, 1, 1)
+
+
+def test_invalid_args_leave_c_untouched(torch_cuda):
+    c = np.full(16, 3.5)
+    a = np.ones(16)
+    lib = _capi.load()
+    assert lib.my_dgemm_ex(4, 4, 4, a.ctypes.data, 3, a.ctypes.data, 4, c.ctypes.data, 4, 0, None) == -5
+    lib.my_dgemm(4, 4, 4, a.ctypes.data, 4, a.ctypes.data, 4, c.ctypes.data, 2)
+    assert lib.my_dgemm_last_status() == -9
+    assert np.all(c == 3.5)
+
+
+def test_c_abi_my_dgemm_host_signature(torch_cuda):
+    m, n, k = 37, 53, 71
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, m + 7, k + 5, m + 3)
+    want = oracle.naive(m, n, k, a, m + 7, b, k + 5, c.copy(), m + 3)
+    lib = _capi.load()
+    got = c.copy()
+    lib.my_dgemm(m, n, k, a.ctypes.data, m + 7, b.ctypes.data, k + 5, got.ctypes.data, m + 3)
+    assert lib.my_dgemm_last_status() == 0
+    rep = oracle.max_abs_diff(got, want, m, n, m + 3, tol=oracle.tolerance(k, 1, 1))
+    assert rep.clean
+    assert np.all(got.reshape(n, m + 3)[:, m:] == -777.25)
+
+
+def test_reference_registry_gate_admits_b200(torch_cuda):
+    from conftest import import_reference, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref (the reference package) not built")
+    gf = import_reference()
+    reg = gf.registry.KernelRegistry()
+    engine.register(reg)  # runs the reference's own validation gate
+    assert "b200" in reg.variant_names()
+    eng = reg.build_engine("b200", None)
+    a, b, c = gf.bench.make_operands(42, 97, 89, 83)
+    want = gf.kernels.gemm_naive(a, b, gf.matrix.copy_matrix(c))
+    got = eng(a, b, gf.matrix.copy_matrix(c))
+    rep = gf.matrix.max_abs_diff(got, want, gf.kernels.tolerance(83, 1.0, 1.0))
+    assert rep.first_bad_i is None
