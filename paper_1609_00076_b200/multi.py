@@ -1,0 +1,146 @@
+"""jc-sharded multi-GPU my_dgemm: one process per GPU, torch.distributed for
+the plumbing, the A broadcast overlapped with the per-rank GEMM chunk by chunk.
+
+Reference mapping.  The reference parallelises loop 3 (ic) or loop 2 (jr)
+over threads with a static, contiguous, balanced split (`split_range`,
+pkg/src/gemmforge/parallel.py:39-57) and never splits pc, because pc
+iterations accumulate into the same C elements (parallel.py:1-12).  Across
+GPUs the natural independent loop is loop 5 (jc, goto.py:212): column j of C
+depends only on A and column j of B.  So:
+
+  * rank g owns the contiguous column panel [j0_g, j1_g) of B and C
+    (`split_columns`, the split_range rule, rounded to the 128-column CTA
+    tile) -- B and C are never communicated;
+  * A (m x k) lives on `root` and is broadcast in k-chunks (`k_chunks`,
+    multiples of 16 = the kernel's K slab, so chunked accumulation is bitwise
+    the single call); chunk i+1 crosses NVLink while chunk i's GEMM runs;
+  * each rank runs C_g += A[:, chunk] * B_g[chunk, :] in ascending chunk
+    order (my_dgemm_shard), the reference's pc order, so C is bitwise
+    identical for every world size.
+
+The compute and broadcast callables are injectable so the host logic runs
+under gloo on CPU in tests (tests/test_multi.py); the product path uses the
+C ABI and NCCL.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+__all__ = ["split_columns", "k_chunks", "ShardPlan", "make_shard_plan", "ShardedDgemm"]
+
+TILE_N = 128
+K_ALIGN = 16
+
+
+def split_columns(n: int, parts: int, align: int = TILE_N) -> tuple[tuple[int, int], ...]:
+    """Contiguous, balanced column panels, earlier ranks taking the larger
+    share (parallel.py:39-57), in units of `align` columns where n allows."""
+    if n < 0:
+        raise ValueError(f"count must be non-negative, got {n}")
+    if parts < 1:
+        raise ValueError(f"workers must be positive, got {parts}")
+    units = -(-n // align)
+    base, rem = divmod(units, parts)
+    out, lo = [], 0
+    for w in range(parts):
+        hi = min(n, lo + (base + (1 if w < rem else 0)) * align)
+        out.append((lo, hi))
+        lo = hi
+    return tuple(out)
+
+
+def k_chunks(k: int, chunk: int) -> tuple[tuple[int, int], ...]:
+    """Ascending k-ranges of `chunk` (rounded up to a multiple of 16)."""
+    if k < 1:
+        raise ValueError(f"k must be positive, got {k}")
+    chunk = max(K_ALIGN, -(-chunk // K_ALIGN) * K_ALIGN)
+    return tuple((p, min(k, p + chunk)) for p in range(0, k, chunk))
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    m: int
+    n: int
+    k: int
+    world: int
+    root: int
+    columns: tuple[tuple[int, int], ...]
+    chunks: tuple[tuple[int, int], ...]
+
+    def local(self, rank: int) -> tuple[int, int]:
+        return self.columns[rank]
+
+
+def make_shard_plan(m: int, n: int, k: int, world: int, root: int = 0,
+                    k_chunk: int = 2048) -> ShardPlan:
+    if min(m, n, k) < 1:
+        raise ValueError(f"matrix dims must be positive, got m={m} n={n} k={k}")
+    if not 0 <= root < world:
+        raise ValueError(f"root {root} outside 0..{world - 1}")
+    chunks = k_chunks(k, k_chunk) if world > 1 else ((0, k),)
+    return ShardPlan(m, n, k, world, root, split_columns(n, world), chunks)
+
+
+def a_span(lda: int, m: int, p0: int, p1: int) -> tuple[int, int]:
+    """Flat element range holding columns [p0, p1) of A: never past the last
+    valid element (matrix.py:58)."""
+    return p0 * lda, (p1 - 1) * lda + m
+
+
+class ShardedDgemm:
+    """Per-rank driver.  `A` is a 1-D buffer of >= (k-1)*lda+m doubles on
+    every rank (the source on root, a receive buffer elsewhere); B_local /
+    C_local hold this rank's column panel (ldb >= k, ldc >= m).
+
+    compute(m, nloc, kc, A_view, lda, B_view, ldb, C_view, ldc) and
+    broadcast(tensor, src) -> handle-with-wait() default to the C ABI on the
+    current CUDA stream and torch.distributed.broadcast(async_op=True).
+    """
+
+    def __init__(self, plan: ShardPlan, rank: int, group=None,
+                 compute: Callable | None = None, broadcast: Callable | None = None,
+                 force_tiled: bool | None = None):
+        self.plan, self.rank, self.group = plan, rank, group
+        # A rank whose panel is one column must not switch to the n==1 kernel
+        # when the global problem is not n==1 (keeps C identical across world
+        # sizes).
+        self.force_tiled = (plan.n > 1) if force_tiled is None else force_tiled
+        self._compute = compute or self._device_compute
+        self._broadcast = broadcast or self._nccl_broadcast
+
+    # -- defaults (GPU) ---------------------------------------------------
+    def _device_compute(self, m, nloc, kc, A, lda, B, ldb, C, ldc):
+        import torch
+
+        from .engine import dgemm_device
+
+        dgemm_device(m, nloc, kc, A.data_ptr(), lda, B.data_ptr(), ldb, C.data_ptr(), ldc,
+                     torch.cuda.current_stream().cuda_stream, force_tiled=self.force_tiled)
+
+    def _nccl_broadcast(self, tensor, src):
+        import torch.distributed as dist
+
+        return dist.broadcast(tensor, src=src, group=self.group, async_op=True)
+
+    # -- one step ---------------------------------------------------------
+    def step(self, A, lda: int, B_local, ldb: int, C_local, ldc: int, broadcast_a: bool = True):
+        p = self.plan
+        j0, j1 = p.local(self.rank)
+        nloc = j1 - j0
+        works = []
+        if p.world > 1 and broadcast_a:
+            for (p0, p1) in p.chunks:
+                lo, hi = a_span(lda, p.m, p0, p1)
+                works.append(self._broadcast(A[lo:hi], p.root))
+        for ci, (p0, p1) in enumerate(p.chunks):
+            if works and self.rank != p.root:
+                works[ci].wait()  # stream-ordered wait on the chunk's arrival
+            if nloc > 0:
+                lo, hi = a_span(lda, p.m, p0, p1)
+                self._compute(p.m, nloc, p1 - p0, A[lo:hi], lda, B_local[p0:], ldb, C_local, ldc)
+        if works and self.rank == p.root:
+            for w in works:
+                w.wait()
+        return C_local

@@ -1,0 +1,125 @@
+"""The drop-in boundary without a GPU: the library builds, loads, exports every
+symbol include/my_dgemm.h declares, and rejects bad arguments before touching
+any memory (reference ValueError semantics, kernels.py:41-49,
+matrix.py:50-53, goto.py:196-204).  No compute is launched here."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1609_00076_b200 import _capi, build, engine
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "my_dgemm.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _capi.load()
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"MY_DGEMM_API\s+[\w\s\*]+?\b(\w+)\s*\(", text)))
+
+
+def test_header_declares_the_baseline_signature():
+    text = open(HEADER).read()
+    assert re.search(r"void my_dgemm\(int m, int n, int k, const double \*A, int lda, "
+                     r"const double \*B, int ldb, double \*C, int ldc\);", text)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    syms = declared_symbols()
+    assert "my_dgemm" in syms and len(syms) >= 10
+    for s in syms:
+        assert hasattr(lib, s), s
+        assert s in _capi.SIGNATURES, f"{s} not typed in _capi.SIGNATURES"
+    # nothing beyond the ABI is exported
+    out = os.popen(f"nm -D --defined-only {_capi.LIB_PATH}").read()
+    exported = {l.split()[-1] for l in out.splitlines() if " T " in l}
+    assert exported == set(syms)
+
+
+def test_library_is_sm100a(lib):
+    out = os.popen(f"cuobjdump --list-elf {_capi.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    sass = os.popen(f"cuobjdump -sass {_capi.LIB_PATH} 2>&1 | grep -c DMMA").read().strip()
+    assert int(sass or 0) > 0, "fast kernel must issue DMMA (FP64 tensor pipe)"
+
+
+def test_version_and_counters(lib):
+    assert b"sm_100a" in lib.my_dgemm_version()
+    assert lib.my_dgemm_kernel_launches() >= 0
+
+
+BAD = [
+    # (m, n, k, lda, ldb, ldc, null index, expected status)
+    (0, 4, 4, 4, 4, 4, None, -1),
+    (4, 0, 4, 4, 4, 4, None, -2),
+    (4, 4, 0, 4, 4, 4, None, -3),
+    (4, 4, 4, 4, 4, 4, 0, -4),
+    (4, 4, 4, 3, 4, 4, None, -5),
+    (4, 4, 4, 4, 4, 4, 1, -6),
+    (4, 4, 4, 4, 3, 4, None, -7),
+    (4, 4, 4, 4, 4, 4, 2, -8),
+    (4, 4, 4, 4, 4, 3, None, -9),
+]
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc,null,status", BAD)
+def test_invalid_arguments_status_and_untouched_c(lib, m, n, k, lda, ldb, ldc, null, status):
+    bufs = [np.full(64, 1.5), np.full(64, 2.5), np.full(64, 3.5)]
+    ptrs = [b.ctypes.data for b in bufs]
+    if null is not None:
+        ptrs[null] = None
+    got = lib.my_dgemm_ex(m, n, k, ptrs[0], lda, ptrs[1], ldb, ptrs[2], ldc, 0, None)
+    assert got == status
+    assert lib.my_dgemm_last_status() == status
+    assert np.all(bufs[2] == 3.5) and np.all(bufs[0] == 1.5)
+    # void entry point records the same status
+    lib.my_dgemm(m, n, k, ptrs[0], lda, ptrs[1], ldb, ptrs[2], ldc)
+    assert lib.my_dgemm_last_status() == status
+
+
+def test_unknown_flags_rejected(lib):
+    a = np.zeros(16)
+    assert lib.my_dgemm_ex(4, 4, 4, a.ctypes.data, 4, a.ctypes.data, 4, a.ctypes.data, 4,
+                           0x100, None) == -10
+
+
+def test_python_boundary_raises_reference_valueerrors(lib):
+    a = engine.alloc_matrix(3, 4)
+    b = engine.alloc_matrix(5, 2)
+    c = engine.alloc_matrix(3, 2)
+    with pytest.raises(ValueError, match="inner dims differ: A is 3x4, B is 5x2"):
+        engine.gemm_b200(a, b, c)
+    b = engine.alloc_matrix(4, 2)
+    with pytest.raises(ValueError, match="C is 3x3, expected 3x2"):
+        engine.gemm_b200(a, b, engine.alloc_matrix(3, 3))
+    with pytest.raises(ValueError, match="leading dimension ld=2 smaller than row count m=3"):
+        engine.Matrix(3, 2, 2, np.zeros(8))
+    with pytest.raises(ValueError, match="buffer too small"):
+        engine.Matrix(3, 2, 5, np.zeros(7))
+    engine.Matrix(3, 2, 5, np.zeros(8))  # exact corner view is legal (matrix.py:58)
+    with pytest.raises(ValueError, match="matrix dims must be positive"):
+        engine.my_dgemm(0, 1, 1, np.zeros(1), 1, np.zeros(1), 1, np.zeros(1), 1)
+    with pytest.raises(ValueError, match="buffer too small"):
+        engine.my_dgemm(4, 4, 4, np.zeros(15), 4, np.zeros(16), 4, np.zeros(16), 4)
+
+
+def test_operand_seed_matches_oracle(lib):
+    import oracle
+
+    for s in [(42, 1, 512, 512, 512), (42, 3, 4093, 4099, 2047), ((1 << 64) - 1, 2, 1, 1, 1)]:
+        assert engine.operand_seed(*s) == oracle.operand_seed(*s)
+
+
+def test_missing_library_fails_loudly(tmp_path, monkeypatch):
+    monkeypatch.setattr(_capi, "_lib", None)
+    with pytest.raises(_capi.NativeLibraryError):
+        _capi.load(str(tmp_path / "absent.so"))
