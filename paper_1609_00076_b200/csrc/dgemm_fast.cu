@@ -25,8 +25,15 @@ namespace fast {
 constexpr int BM = 128;          // CTA tile rows (m)
 constexpr int BN = 128;          // CTA tile cols (n)
 constexpr int BK = 16;           // K slab per pipeline stage
-constexpr int STAGES = 4;        // cp.async ring depth
-constexpr int THREADS = 256;     // 8 warps: 2 (m) x 4 (n)
+constexpr int STAGES = 5;        // cp.async ring depth
+constexpr int CONSUMER_WARPS = 8;  // 2 (m) x 4 (n) DMMA warps: 2 per SM sub-partition
+constexpr int PRODUCER_WARPS = 4;  // one staging warp per sub-partition
+constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
+// Register split per sub-partition (16K regs): 1 producer + 2 consumers.
+// Launch at 168 (12 warps x 168 x 32 <= 64K), then setmaxnreg moves
+// producers down to 40 and consumers up to 232 (40 + 2*232 <= 512).
+constexpr int PRODUCER_REGS = 40;
+constexpr int CONSUMER_REGS = 232;
 constexpr int WM = 64, WN = 32;  // warp tile
 constexpr int FM = WM / 8, FN = WN / 8;
 // Padded pitches make every fragment load and every 16-byte staging store
@@ -42,6 +49,13 @@ constexpr int GROUP_M = 8;
 
 // VEC doubles per cp.async (2: 16-byte copies, needs even ld and 16-B aligned
 // bases; 1: 8-byte copies for odd leading dimensions / 8-B aligned views).
+//
+// Warp roles: warps 0..7 are consumers (DMMA micro-tiles, 2 per SM
+// sub-partition); warp 8 is the producer that stages every K slab with
+// cp.async and signals slab arrival on full[s] (cp.async.mbarrier.arrive).
+// Consumers release a slab on empty[s] when their fragments are in
+// registers.  No CTA-wide barrier in the main loop: each consumer warp runs
+// at its own pace, bounded only by the STAGES-deep ring.
 template <int VEC>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
@@ -50,6 +64,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   extern __shared__ __align__(128) double smem[];
   double *As = smem;
   double *Bs = smem + STAGES * A_STAGE;
+  __shared__ __align__(8) uint64_t full_bar[STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[STAGES];
 
   // Grouped raster: GROUP_M tile-rows per band, column-major inside a band.
   const int bid = blockIdx.x;
@@ -62,53 +78,75 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int r = lane >> 2, q = lane & 3;
-
   const int KT = (K + BK - 1) / BK;
 
-  // ---- staging (pack_a / pack_b equivalent) ----
-  auto load_stage = [&](int slot, int kt) {
-    const int kbase = kt * BK;
-    double *as = As + slot * A_STAGE;
-    double *bs = Bs + slot * B_STAGE;
-    constexpr int A_COPIES = BK * BM / VEC / THREADS;
+  if (tid == 0) {
 #pragma unroll
-    for (int c = 0; c < A_COPIES; ++c) {
-      const int e = (tid + c * THREADS) * VEC;
-      const int kk = e / BM, mm = e % BM;
-      const int gk = kbase + kk, gmr = m0 + mm;
-      int bytes = 0;
-      const double *src = A;
-      if (gk < K && gmr < M) {
-        bytes = min(VEC, M - gmr) * 8;
-        src = A + (int64_t)gk * lda + gmr;
-      }
-      cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], PRODUCER_WARPS * 32);  // every producer lane
+      mbar_init(&empty_bar[s], CONSUMER_WARPS);      // one arrival per consumer warp
     }
-    constexpr int B_COPIES = BK * BN / VEC / THREADS;
-#pragma unroll
-    for (int c = 0; c < B_COPIES; ++c) {
-      const int e = (tid + c * THREADS) * VEC;
-      const int nn = e / BK, kk = e % BK;
-      const int gk = kbase + kk, gn = n0 + nn;
-      int bytes = 0;
-      const double *src = B;
-      if (gn < N && gk < K) {
-        bytes = min(VEC, K - gk) * 8;
-        src = B + (int64_t)gn * ldb + gk;
-      }
-      cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
-    }
-  };
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
-  // ---- prologue: start the ring, then load C into the accumulators ----
+  if (warp >= CONSUMER_WARPS) {
+    // ================= producers: pack_a / pack_b equivalent =================
+    // One producer warp per SM sub-partition; registers handed to consumers.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+    const int pw = warp - CONSUMER_WARPS;
+    for (int kt = 0; kt < KT; ++kt) {
+      const int slot = kt % STAGES;
+      if (kt >= STAGES) mbar_wait(&empty_bar[slot], ((kt / STAGES) - 1) & 1);
+      const int kbase = kt * BK;
+      double *as = As + slot * A_STAGE;
+      double *bs = Bs + slot * B_STAGE;
+      // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
+      // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_async_commit();
+      for (int i = 0; i < BK * BM / (VEC * 32 * PRODUCER_WARPS); ++i) {
+        const int e = ((pw * 32 + lane) + i * 32 * PRODUCER_WARPS) * VEC;
+        const int kk = e / BM, mm = e % BM;
+        const int gk = kbase + kk, gmr = m0 + mm;
+        int bytes = 0;
+        const double *src = A;
+        if (gk < K && gmr < M) {
+          bytes = min(VEC, M - gmr) * 8;
+          src = A + (int64_t)gk * lda + gmr;
+        }
+        cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
+      }
+      // B slab [BN][BK], k contiguous: producer pw owns n-rows [32pw, 32pw+32);
+      // a quarter-warp writes 4 rows x 2 chunks (conflict-free at pitch BP).
+#pragma unroll
+      for (int i = 0; i < BK * 32 / (VEC * 32); ++i) {
+        int nn, kk;
+        if constexpr (VEC == 2) {
+          nn = pw * 32 + (lane >> 1) + 16 * (i >> 2);
+          kk = 2 * ((lane & 1) + 2 * (i & 3));
+        } else {
+          nn = pw * 32 + (lane >> 2) + 8 * (i >> 2);
+          kk = (lane & 3) + 4 * (i & 3);
+        }
+        const int gk = kbase + kk, gn = n0 + nn;
+        int bytes = 0;
+        const double *src = B;
+        if (gn < N && gk < K) {
+          bytes = min(VEC, K - gk) * 8;
+          src = B + (int64_t)gn * ldb + gk;
+        }
+        cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
+      }
+      cp_async_mbar_arrive(&full_bar[slot]);
+    }
+    cp_async_wait<0>();
+    return;
   }
 
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+  // ================= consumers: loops 2/1 + micro-kernel =================
+  const int wm = warp & 1, wn = warp >> 1;
+  const int r = lane >> 2, q = lane & 3;
   double acc[FM][FN][2];
   const int row0 = m0 + wm * WM + r;
   const int col0 = n0 + wn * WN + 2 * q;
@@ -122,35 +160,41 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         acc[i][j][e] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
       }
 
-  // Per-thread fragment offsets inside a stage.
-  const int a_off = q * AP + wm * WM + r;  // + kk*4*AP + i*8
+  const int a_off = q * AP + wm * WM + r;    // + kk*4*AP + i*8
   const int b_off = (wn * WN + r) * BP + q;  // + j*8*BP + kk*4
+  double fa[2][FM], fb[2][FN];
+  auto load_frags = [&](int buf, int slot, int kk) {
+    const double *as = As + slot * A_STAGE + a_off + kk * 4 * AP;
+    const double *bs = Bs + slot * B_STAGE + b_off + kk * 4;
+#pragma unroll
+    for (int i = 0; i < FM; ++i) fa[buf][i] = as[i * 8];
+#pragma unroll
+    for (int j = 0; j < FN; ++j) fb[buf][j] = bs[j * 8 * BP];
+  };
 
-  // ---- main loop (loop 4, pc) ----
+  mbar_wait(&full_bar[0], 0);
+  load_frags(0, 0, 0);
   for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nk = kt + STAGES - 1;
-      if (nk < KT) load_stage(nk % STAGES, nk);
-      cp_async_commit();
-    }
-    const double *as = As + (kt % STAGES) * A_STAGE + a_off;
-    const double *bs = Bs + (kt % STAGES) * B_STAGE + b_off;
+    const int slot = kt % STAGES;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[FM], b[FN];
-#pragma unroll
-      for (int i = 0; i < FM; ++i) a[i] = as[kk * 4 * AP + i * 8];
-#pragma unroll
-      for (int j = 0; j < FN; ++j) b[j] = bs[j * 8 * BP + kk * 4];
+      const int cur = kk & 1;
+      if (kk + 1 < BK / 4) {
+        load_frags(cur ^ 1, slot, kk + 1);
+      } else if (kt + 1 < KT) {
+        const int nslot = (kt + 1) % STAGES;
+        mbar_wait(&full_bar[nslot], ((kt + 1) / STAGES) & 1);
+        load_frags(cur ^ 1, nslot, 0);
+      }
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fa[cur][i], fb[cur][j]);
     }
+    // every fragment of this slab has been consumed by an issued DMMA
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
   }
-  cp_async_wait<0>();
 
   // ---- epilogue: valid region only (padding rows never touched) ----
 #pragma unroll
