@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmy_dgemm_b200.so")
+LIB_PATH = os.environ.get("MY_DGEMM_LIB") or os.path.join(HERE, "libmy_dgemm_b200.so")
 
 # Flags (include/my_dgemm.h)
 DEVICE_PTRS = 0x1

@@ -41,13 +41,50 @@ MYD_DEVICE void mbar_init(uint64_t *bar, uint32_t count) {
 }
 
 MYD_DEVICE void mbar_arrive(uint64_t *bar) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Single non-blocking probe; issue early, consume the result later so the
+// probe latency overlaps independent work.
+MYD_DEVICE bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 
 // Arrive on `bar` once every cp.async this thread issued so far has landed.
 // .noinc: the arrival counts against the count given at init.
 MYD_DEVICE void cp_async_mbar_arrive(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Tracks this thread's prior cp.async ops: +1 pending now, -1 when they land.
+MYD_DEVICE void cp_async_mbar_arrive_inc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// One arrival plus `bytes` of expected async-proxy transactions.
+MYD_DEVICE void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+// Bulk (TMA-engine) copy of `bytes` contiguous bytes global -> shared,
+// completion counted on `bar` (complete_tx).  16-byte aligned src/dst,
+// bytes a multiple of 16.
+MYD_DEVICE void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 MYD_DEVICE void mbar_wait(uint64_t *bar, uint32_t parity) {

@@ -17,21 +17,46 @@
 //                         (tools/microbench/fp64_peak.cu, profiles/).
 // C is loaded into the accumulators first, like _mk's tile load
 // (_ckernels.pyx:28-32), and only the valid region is stored back.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace myd {
 
+#ifdef MYD_FAST_PROFILE
+// [0] consumer slow-wait cycles, [1] consumer slow waits, [2] producer empty-wait cycles,
+// [3] producer waits, [4] consumer first-slab wait cycles, [5] consumer total loop cycles,
+// [6] producer issue cycles
+__device__ unsigned long long g_fast_prof[8];
+#define PROF_T0() long long _pt0 = clock64()
+#define PROF_ADD(i, v) atomicAdd(&g_fast_prof[i], (unsigned long long)(v))
+#else
+#define PROF_T0()
+#define PROF_ADD(i, v)
+#endif
+
 namespace fast {
 constexpr int BM = 128;          // CTA tile rows (m)
 constexpr int BN = 128;          // CTA tile cols (n)
-constexpr int BK = 16;           // K slab per pipeline stage
-constexpr int STAGES = 5;        // cp.async ring depth
+#ifndef MYD_FAST_BK
+#define MYD_FAST_BK 16
+#endif
+#ifndef MYD_FAST_STAGES
+#define MYD_FAST_STAGES 5
+#endif
+#ifndef MYD_FAST_GROUP_M
+#define MYD_FAST_GROUP_M 8
+#endif
+constexpr int BK = MYD_FAST_BK;          // K slab per pipeline stage
+constexpr int STAGES = MYD_FAST_STAGES;  // cp.async ring depth
 constexpr int CONSUMER_WARPS = 8;  // 2 (m) x 4 (n) DMMA warps: 2 per SM sub-partition
 constexpr int PRODUCER_WARPS = 4;  // one staging warp per sub-partition
 constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
 // Register split per sub-partition (16K regs): 1 producer + 2 consumers.
 // Launch at 168 (12 warps x 168 x 32 <= 64K), then setmaxnreg moves
-// producers down to 40 and consumers up to 232 (40 + 2*232 <= 512).
+// producers down to 40 and consumers up to 232: the CTA keeps the 168 x 384
+// registers it launched with (40*128 + 232*256 = 168*384); asking for more
+// would block setmaxnreg.inc forever.
 constexpr int PRODUCER_REGS = 40;
 constexpr int CONSUMER_REGS = 232;
 constexpr int WM = 64, WN = 32;  // warp tile
@@ -44,7 +69,14 @@ constexpr int BP = BK + 4;  // B slab: [BN][BP]   (k contiguous, as in HBM)
 constexpr int A_STAGE = BK * AP;
 constexpr int B_STAGE = BN * BP;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
-constexpr int GROUP_M = 8;
+constexpr int GROUP_M = MYD_FAST_GROUP_M;
+constexpr int KSTEPS = BK / 4;                  // DMMA k-steps per slab
+constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier is probed
+constexpr int PROBE_STEP_ALT = KSTEPS - 1;      // ... by the second warp of each sub-partition
+#ifndef MYD_FAST_STAGGER
+#define MYD_FAST_STAGGER 0
+#endif
+constexpr bool STAGGER = MYD_FAST_STAGGER != 0;
 }  // namespace fast
 
 // VEC doubles per cp.async (2: 16-byte copies, needs even ld and 16-B aligned
@@ -83,7 +115,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], PRODUCER_WARPS * 32);  // every producer lane
+      mbar_init(&full_bar[s], PRODUCER_WARPS);       // one arrival per producer warp
       mbar_init(&empty_bar[s], CONSUMER_WARPS);      // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -95,12 +127,34 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     // One producer warp per SM sub-partition; registers handed to consumers.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
+    // Interior tiles with 16-byte aligned operands use the bulk-copy (TMA)
+    // engine: one cp.async.bulk per A k-row (BM*8 bytes) and per B column
+    // segment (BK*8 bytes), straight into the padded slab layout, no LSU
+    // traffic.  Edge tiles and a ragged last slab use zero-filling LDGSTS.
+    const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
     for (int kt = 0; kt < KT; ++kt) {
       const int slot = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(&empty_bar[slot], ((kt / STAGES) - 1) & 1);
+      if (kt >= STAGES) {
+        PROF_T0();
+        mbar_wait(&empty_bar[slot], ((kt / STAGES) - 1) & 1);
+        if (lane == 0) { PROF_ADD(2, clock64() - _pt0); PROF_ADD(3, 1); }
+      }
       const int kbase = kt * BK;
       double *as = As + slot * A_STAGE;
       double *bs = Bs + slot * B_STAGE;
+      if (interior && kbase + BK <= K) {
+        constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
+        constexpr uint32_t BYTES = (A_ROWS * BM + 32 * BK) * 8;
+        if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
+        __syncwarp();
+        if (lane < A_ROWS) {
+          const int kk = pw * A_ROWS + lane;
+          bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
+        }
+        const int nn = pw * 32 + lane;
+        bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+        continue;
+      }
       // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
       // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
 #pragma unroll
@@ -121,12 +175,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < BK * 32 / (VEC * 32); ++i) {
         int nn, kk;
-        if constexpr (VEC == 2) {
-          nn = pw * 32 + (lane >> 1) + 16 * (i >> 2);
-          kk = 2 * ((lane & 1) + 2 * (i & 3));
-        } else {
-          nn = pw * 32 + (lane >> 2) + 8 * (i >> 2);
-          kk = (lane & 3) + 4 * (i & 3);
+        if constexpr (VEC == 2) {  // 16 rows x 2 chunks per instruction
+          nn = pw * 32 + (lane >> 1) + 16 * (i / (BK / 4));
+          kk = 2 * ((lane & 1) + 2 * (i % (BK / 4)));
+        } else {  // 8 rows x 4 doubles per instruction
+          nn = pw * 32 + (lane >> 2) + 8 * (i / (BK / 4));
+          kk = (lane & 3) + 4 * (i % (BK / 4));
         }
         const int gk = kbase + kk, gn = n0 + nn;
         int bytes = 0;
@@ -137,7 +191,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         }
         cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
       }
-      cp_async_mbar_arrive(&full_bar[slot]);
+      // full_bar counts one arrival per producer warp; each lane's copies are
+      // tracked by its own pending +1/-1 (cp.async.mbarrier.arrive).
+      cp_async_mbar_arrive_inc(&full_bar[slot]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[slot]);
     }
     cp_async_wait<0>();
     return;
@@ -172,18 +230,35 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     for (int j = 0; j < FN; ++j) fb[buf][j] = bs[j * 8 * BP];
   };
 
-  mbar_wait(&full_bar[0], 0);
+#ifdef MYD_FAST_PROFILE
+  long long loop_t0 = clock64();
+#endif
+  {
+    PROF_T0();
+    mbar_wait(&full_bar[0], 0);
+    if (lane == 0) PROF_ADD(4, clock64() - _pt0);
+  }
   load_frags(0, 0, 0);
+  auto main_loop = [&](auto probe_c) {
+  constexpr int PROBE = decltype(probe_c)::value;
   for (int kt = 0; kt < KT; ++kt) {
     const int slot = kt % STAGES;
+    const int nslot = (kt + 1) % STAGES;
+    const uint32_t nparity = ((kt + 1) / STAGES) & 1;
+    bool next_ready = true;
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
+    for (int kk = 0; kk < KSTEPS; ++kk) {
       const int cur = kk & 1;
-      if (kk + 1 < BK / 4) {
+      // Probe the next slab's barrier early; its latency hides behind DMMAs.
+      if (kk == PROBE && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
+      if (kk + 1 < KSTEPS) {
         load_frags(cur ^ 1, slot, kk + 1);
       } else if (kt + 1 < KT) {
-        const int nslot = (kt + 1) % STAGES;
-        mbar_wait(&full_bar[nslot], ((kt + 1) / STAGES) & 1);
+        if (!next_ready) {
+          PROF_T0();
+          mbar_wait(&full_bar[nslot], nparity);
+          if (lane == 0) { PROF_ADD(0, clock64() - _pt0); PROF_ADD(1, 1); }
+        }
         load_frags(cur ^ 1, nslot, 0);
       }
 #pragma unroll
@@ -195,7 +270,15 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);
   }
+  };
+  // The two consumer warps of a sub-partition (w, w+4) probe at different
+  // k-steps so their probe latencies do not coincide.
+  if (STAGGER && (warp & 4)) main_loop(std::integral_constant<int, PROBE_STEP_ALT>{});
+  else main_loop(std::integral_constant<int, PROBE_STEP>{});
 
+#ifdef MYD_FAST_PROFILE
+  if (lane == 0) PROF_ADD(5, clock64() - loop_t0);
+#endif
   // ---- epilogue: valid region only (padding rows never touched) ----
 #pragma unroll
   for (int i = 0; i < FM; ++i)
@@ -232,3 +315,13 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
 }
 
 }  // namespace myd
+
+#ifdef MYD_FAST_PROFILE
+extern "C" __attribute__((visibility("default"))) void my_dgemm_fast_profile(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, myd::g_fast_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(myd::g_fast_prof, z, sizeof z);
+  }
+}
+#endif
