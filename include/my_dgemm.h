@@ -44,6 +44,8 @@ extern "C" {
 #define MY_DGEMM_EXACT 0x2u       /* bitwise twin of the reference oracle (verification) */
 #define MY_DGEMM_FORCE_TILED 0x4u /* bypass the m==1 / n==1 bandwidth kernels */
 #define MY_DGEMM_FORCE_VEC1 0x8u  /* force 8-byte operand staging (odd-ld path) */
+#define MY_DGEMM_FORCE_STRIPS2 0x10u /* run every tile as two 128x64 strips (tests) */
+#define MY_DGEMM_FORCE_STRIPS4 0x20u /* run every tile as four 128x32 strips (tests) */
 
 /*
  * The BASELINE.json north_star signature.  Replaces the reference's

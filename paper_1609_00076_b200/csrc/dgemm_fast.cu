@@ -4,19 +4,30 @@
 // _ckernels.pyx:15-45,142-195) re-derived for Blackwell:
 //   loop 5/3 (jc, ic)  -> the CTA grid over 128x128 tiles of C, rastered in
 //                         bands of GROUP_M tile-rows so co-resident CTAs share
-//                         A and B panels in the 126 MB L2;
+//                         A and B panels in the 126 MB L2; the last partial
+//                         wave is re-cut into 128x64 / 128x32 strips so every
+//                         SM gets work (launch_dgemm_fast);
 //   loop 4 (pc)        -> the in-CTA K loop over BK=16 slabs;
-//   pack_a / pack_b    -> cp.async (LDGSTS) staging of the A and B slabs into a
-//                         STAGES-deep shared-memory ring; zero-fill of the
-//                         out-of-range lanes replaces the zero-padded panels;
-//                         no separate pack pass touches HBM;
-//   loops 2/1 + _mk    -> 8 warps, each a 64x32 register tile of C built from
-//                         8x4 DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
+//   pack_a / pack_b    -> producer warps stage each A and B slab into a
+//                         STAGES-deep shared-memory ring: bulk copies by the
+//                         TMA engine (cp.async.bulk, one per A k-row and per
+//                         B column segment) for interior tiles, zero-filling
+//                         cp.async (LDGSTS) at the edges; no pack pass touches
+//                         HBM;
+//   loops 2/1 + _mk    -> 8 consumer warps, each a register tile of C built
+//                         from DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
 //                         no tcgen05 kind on sm_100a; the DMMA pipe measured
 //                         37.1 TFLOP/s (128 flop/clk/SM) vs 34.0 for DFMA
-//                         (tools/microbench/fp64_peak.cu, profiles/).
+//                         (profiles/fp64_peak_r01.txt).
 // C is loaded into the accumulators first, like _mk's tile load
 // (_ckernels.pyx:28-32), and only the valid region is stored back.
+//
+// Per-element arithmetic (k grouped in fours from p = 0, one DMMA per group,
+// groups in ascending order, accumulator starting at C) does not depend on
+// the CTA width, the tile position or the launch plan, so every plan and
+// every k-chunking at multiples of 16 gives bitwise the same C.
+#include <algorithm>
+#include <atomic>
 #include <type_traits>
 
 #include "common.cuh"
@@ -25,8 +36,7 @@ namespace myd {
 
 #ifdef MYD_FAST_PROFILE
 // [0] consumer slow-wait cycles, [1] consumer slow waits, [2] producer empty-wait cycles,
-// [3] producer waits, [4] consumer first-slab wait cycles, [5] consumer total loop cycles,
-// [6] producer issue cycles
+// [3] producer waits, [4] consumer first-slab wait cycles, [5] consumer total loop cycles
 __device__ unsigned long long g_fast_prof[8];
 #define PROF_T0() long long _pt0 = clock64()
 #define PROF_ADD(i, v) atomicAdd(&g_fast_prof[i], (unsigned long long)(v))
@@ -36,8 +46,6 @@ __device__ unsigned long long g_fast_prof[8];
 #endif
 
 namespace fast {
-constexpr int BM = 128;          // CTA tile rows (m)
-constexpr int BN = 128;          // CTA tile cols (n)
 #ifndef MYD_FAST_BK
 #define MYD_FAST_BK 16
 #endif
@@ -47,10 +55,12 @@ constexpr int BN = 128;          // CTA tile cols (n)
 #ifndef MYD_FAST_GROUP_M
 #define MYD_FAST_GROUP_M 8
 #endif
+constexpr int BM = 128;                  // CTA tile rows (m)
+constexpr int TILE_N = 128;              // full CTA tile cols (n); strips are TILE_N / split wide
 constexpr int BK = MYD_FAST_BK;          // K slab per pipeline stage
-constexpr int STAGES = MYD_FAST_STAGES;  // cp.async ring depth
-constexpr int CONSUMER_WARPS = 8;  // 2 (m) x 4 (n) DMMA warps: 2 per SM sub-partition
-constexpr int PRODUCER_WARPS = 4;  // one staging warp per sub-partition
+constexpr int STAGES = MYD_FAST_STAGES;  // ring depth
+constexpr int CONSUMER_WARPS = 8;        // 2 per SM sub-partition
+constexpr int PRODUCER_WARPS = 4;        // one staging warp per sub-partition
 constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
 // Register split per sub-partition (16K regs): 1 producer + 2 consumers.
 // Launch at 168 (12 warps x 168 x 32 <= 64K), then setmaxnreg moves
@@ -59,54 +69,60 @@ constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
 // would block setmaxnreg.inc forever.
 constexpr int PRODUCER_REGS = 40;
 constexpr int CONSUMER_REGS = 232;
-constexpr int WM = 64, WN = 32;  // warp tile
-constexpr int FM = WM / 8, FN = WN / 8;
+constexpr int WN = 32;  // warp tile width (4 DMMA column fragments)
 // Padded pitches make every fragment load and every 16-byte staging store
 // conflict-free: a half-warp's 4 k-rows of A (4 n-rows of B) land in 4
 // distinct 32-byte bank groups (pitch = 4 mod 16 doubles).
 constexpr int AP = BM + 4;  // A slab: [BK][AP]   (m contiguous, as in HBM)
 constexpr int BP = BK + 4;  // B slab: [BN][BP]   (k contiguous, as in HBM)
 constexpr int A_STAGE = BK * AP;
-constexpr int B_STAGE = BN * BP;
+constexpr int B_STAGE = TILE_N * BP;  // sized for the widest CTA
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
 constexpr int GROUP_M = MYD_FAST_GROUP_M;
 constexpr int KSTEPS = BK / 4;                  // DMMA k-steps per slab
 constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier is probed
-constexpr int PROBE_STEP_ALT = KSTEPS - 1;      // ... by the second warp of each sub-partition
-#ifndef MYD_FAST_STAGGER
-#define MYD_FAST_STAGGER 0
-#endif
-constexpr bool STAGGER = MYD_FAST_STAGGER != 0;
 }  // namespace fast
 
-// VEC doubles per cp.async (2: 16-byte copies, needs even ld and 16-B aligned
-// bases; 1: 8-byte copies for odd leading dimensions / 8-B aligned views).
+// VEC: doubles per LDGSTS (2: 16-byte copies and the bulk path, needs even
+// ld and 16-B aligned bases; 1: 8-byte copies for odd ld / 8-B aligned views).
+// BN: CTA width (128 full tiles; 64 / 32 tail strips).  Warps tile the CTA as
+// (8 / (BN/32)) x (BN/32) with 32-column warp tiles, so all 8 consumer warps
+// work whatever the width.
 //
-// Warp roles: warps 0..7 are consumers (DMMA micro-tiles, 2 per SM
-// sub-partition); warp 8 is the producer that stages every K slab with
-// cp.async and signals slab arrival on full[s] (cp.async.mbarrier.arrive).
-// Consumers release a slab on empty[s] when their fragments are in
-// registers.  No CTA-wide barrier in the main loop: each consumer warp runs
-// at its own pace, bounded only by the STAGES-deep ring.
-template <int VEC>
+// Warp roles: warps 0..7 consume (DMMA), warps 8..11 produce (staging).
+// full[s] completes when slab s has landed (bulk-copy transaction bytes or
+// LDGSTS completions); empty[s] when all 8 consumers have their fragments of
+// slab s in registers.  No CTA-wide barrier in the main loop.
+template <int VEC, int BN>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
-                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n) {
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0) {
   using namespace fast;
+  constexpr int SPLIT = TILE_N / BN;
+  constexpr int WARPS_N = BN / WN;
+  constexpr int WARPS_M = CONSUMER_WARPS / WARPS_N;
+  constexpr int WM = BM / WARPS_M;
+  constexpr int FM = WM / 8, FN = WN / 8;
+  constexpr int RW = BN / PRODUCER_WARPS;  // B rows staged by each producer warp
+  static_assert(WARPS_M * WARPS_N == CONSUMER_WARPS && FM >= 1 && RW >= 8, "tile shape");
+
   extern __shared__ __align__(128) double smem[];
   double *As = smem;
   double *Bs = smem + STAGES * A_STAGE;
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
 
-  // Grouped raster: GROUP_M tile-rows per band, column-major inside a band.
-  const int bid = blockIdx.x;
+  // Grouped raster over full tiles: GROUP_M tile-rows per band, column-major
+  // inside a band.  Strip launches cut tile (tile0 + bid/SPLIT) into SPLIT
+  // column strips.
+  const int tile = tile0 + (int)(blockIdx.x / SPLIT);
+  const int strip = (int)(blockIdx.x % SPLIT);
   const int band = GROUP_M * tiles_n;
-  const int first_m = (bid / band) * GROUP_M;
+  const int first_m = (tile / band) * GROUP_M;
   const int gm = min(tiles_m - first_m, GROUP_M);
-  const int tm = first_m + (bid % band) % gm;
-  const int tn = (bid % band) / gm;
-  const int m0 = tm * BM, n0 = tn * BN;
+  const int tm = first_m + (tile % band) % gm;
+  const int tn = (tile % band) / gm;
+  const int m0 = tm * BM, n0 = tn * TILE_N + strip * BN;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -115,8 +131,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   if (tid == 0) {
 #pragma unroll
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], PRODUCER_WARPS);       // one arrival per producer warp
-      mbar_init(&empty_bar[s], CONSUMER_WARPS);      // one arrival per consumer warp
+      mbar_init(&full_bar[s], PRODUCER_WARPS);   // one arrival per producer warp
+      mbar_init(&empty_bar[s], CONSUMER_WARPS);  // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -124,35 +140,38 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   if (warp >= CONSUMER_WARPS) {
     // ================= producers: pack_a / pack_b equivalent =================
-    // One producer warp per SM sub-partition; registers handed to consumers.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
     // Interior tiles with 16-byte aligned operands use the bulk-copy (TMA)
-    // engine: one cp.async.bulk per A k-row (BM*8 bytes) and per B column
-    // segment (BK*8 bytes), straight into the padded slab layout, no LSU
-    // traffic.  Edge tiles and a ragged last slab use zero-filling LDGSTS.
+    // engine straight into the padded slab layout, with no LSU traffic.
+    // Edge tiles and a ragged last slab use zero-filling LDGSTS.
     const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
     for (int kt = 0; kt < KT; ++kt) {
       const int slot = kt % STAGES;
       if (kt >= STAGES) {
         PROF_T0();
         mbar_wait(&empty_bar[slot], ((kt / STAGES) - 1) & 1);
-        if (lane == 0) { PROF_ADD(2, clock64() - _pt0); PROF_ADD(3, 1); }
+        if (lane == 0) {
+          PROF_ADD(2, clock64() - _pt0);
+          PROF_ADD(3, 1);
+        }
       }
       const int kbase = kt * BK;
       double *as = As + slot * A_STAGE;
       double *bs = Bs + slot * B_STAGE;
       if (interior && kbase + BK <= K) {
         constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
-        constexpr uint32_t BYTES = (A_ROWS * BM + 32 * BK) * 8;
+        constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
         if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
         __syncwarp();
         if (lane < A_ROWS) {
           const int kk = pw * A_ROWS + lane;
           bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
         }
-        const int nn = pw * 32 + lane;
-        bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+        if (lane < RW) {
+          const int nn = pw * RW + lane;
+          bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+        }
         continue;
       }
       // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
@@ -170,17 +189,18 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         }
         cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
       }
-      // B slab [BN][BK], k contiguous: producer pw owns n-rows [32pw, 32pw+32);
-      // a quarter-warp writes 4 rows x 2 chunks (conflict-free at pitch BP).
+      // B slab [BN][BK], k contiguous: producer pw owns rows [RW*pw, RW*pw+RW).
+      // VEC=2: a quarter-warp writes 4 rows x 2 chunks (conflict-free at BP).
 #pragma unroll
-      for (int i = 0; i < BK * 32 / (VEC * 32); ++i) {
+      for (int i = 0; i < RW * BK / (VEC * 32); ++i) {
+        const int idx = i * 32 + lane;
         int nn, kk;
-        if constexpr (VEC == 2) {  // 16 rows x 2 chunks per instruction
-          nn = pw * 32 + (lane >> 1) + 16 * (i / (BK / 4));
-          kk = 2 * ((lane & 1) + 2 * (i % (BK / 4)));
-        } else {  // 8 rows x 4 doubles per instruction
-          nn = pw * 32 + (lane >> 2) + 8 * (i / (BK / 4));
-          kk = (lane & 3) + 4 * (i % (BK / 4));
+        if constexpr (VEC == 2) {
+          nn = pw * RW + (idx >> 1) % RW;
+          kk = 2 * (((idx >> 1) / RW) * 2 + (idx & 1));
+        } else {
+          nn = pw * RW + (idx >> 2) % RW;
+          kk = ((idx >> 2) / RW) * 4 + (idx & 3);
         }
         const int gk = kbase + kk, gn = n0 + nn;
         int bytes = 0;
@@ -203,7 +223,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
   // ================= consumers: loops 2/1 + micro-kernel =================
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int r = lane >> 2, q = lane & 3;
   double acc[FM][FN][2];
   const int row0 = m0 + wm * WM + r;
@@ -239,8 +259,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (lane == 0) PROF_ADD(4, clock64() - _pt0);
   }
   load_frags(0, 0, 0);
-  auto main_loop = [&](auto probe_c) {
-  constexpr int PROBE = decltype(probe_c)::value;
   for (int kt = 0; kt < KT; ++kt) {
     const int slot = kt % STAGES;
     const int nslot = (kt + 1) % STAGES;
@@ -250,14 +268,17 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     for (int kk = 0; kk < KSTEPS; ++kk) {
       const int cur = kk & 1;
       // Probe the next slab's barrier early; its latency hides behind DMMAs.
-      if (kk == PROBE && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
+      if (kk == PROBE_STEP && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
       if (kk + 1 < KSTEPS) {
         load_frags(cur ^ 1, slot, kk + 1);
       } else if (kt + 1 < KT) {
         if (!next_ready) {
           PROF_T0();
           mbar_wait(&full_bar[nslot], nparity);
-          if (lane == 0) { PROF_ADD(0, clock64() - _pt0); PROF_ADD(1, 1); }
+          if (lane == 0) {
+            PROF_ADD(0, clock64() - _pt0);
+            PROF_ADD(1, 1);
+          }
         }
         load_frags(cur ^ 1, nslot, 0);
       }
@@ -270,11 +291,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[slot]);
   }
-  };
-  // The two consumer warps of a sub-partition (w, w+4) probe at different
-  // k-steps so their probe latencies do not coincide.
-  if (STAGGER && (warp & 4)) main_loop(std::integral_constant<int, PROBE_STEP_ALT>{});
-  else main_loop(std::integral_constant<int, PROBE_STEP>{});
 
 #ifdef MYD_FAST_PROFILE
   if (lane == 0) PROF_ADD(5, clock64() - loop_t0);
@@ -291,27 +307,96 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       }
 }
 
-cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
-                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1) {
+namespace {
+
+template <int VEC, int BN>
+cudaError_t launch_one(unsigned grid, int M, int N, int K, const double *A, int64_t lda, const double *B,
+                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, cudaStream_t st) {
   using namespace fast;
-  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-  const long long tiles = (long long)tiles_m * tiles_n;
-  if (tiles > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  const bool aligned16 = (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
-  // Set on every call: cheap, per-device, and thread-safe without a flag.
-  if (aligned16 && !force_vec1) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  // The opt-in shared-memory size is a per-device function attribute: set it
+  // once per (device, instantiation); racing first calls just set it twice.
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e =
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    dgemm_fast_kernel<2><<<(unsigned)tiles, THREADS, SMEM_BYTES, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
-                                                                           tiles_n);
-  } else {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    dgemm_fast_kernel<1><<<(unsigned)tiles, THREADS, SMEM_BYTES, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
-                                                                           tiles_n);
+    attr_done.fetch_or(bit, std::memory_order_release);
   }
+  dgemm_fast_kernel<VEC, BN>
+      <<<grid, THREADS, SMEM_BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int VEC>
+cudaError_t launch_split(int split, unsigned grid, int M, int N, int K, const double *A, int64_t lda,
+                         const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                         cudaStream_t st) {
+  switch (split) {
+    case 1: return launch_one<VEC, 128>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 2: return launch_one<VEC, 64>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    default: return launch_one<VEC, 32>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+  }
+}
+
+int sm_count() {
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int v = cached[dev & 63].load(std::memory_order_relaxed);
+  if (v <= 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+    cached[dev & 63].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+}  // namespace
+
+// Launch plan.  With G SMs (one CTA each) and T full tiles, T = q*G + r:
+// the first q*G tiles run as full 128x128 tiles; the r leftovers are cut into
+// `split` column strips (128x64 or 128x32, still 8 busy warps) when that
+// shortens the last wave: its cost is ceil(r*split/G)/split tile-times.
+// force_split (0 = plan) pins the strip width for tests.
+cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split) {
+  using namespace fast;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + TILE_N - 1) / TILE_N;
+  const long long tiles = (long long)tiles_m * tiles_n;
+  if (tiles > 0x7fffffffLL / 4) return cudaErrorInvalidConfiguration;
+  const bool vec2 =
+      !force_vec1 && (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  const long long G = sm_count();
+  long long q = tiles / G, r = tiles % G;
+  int split = 1;
+  if (force_split > 1) {
+    split = force_split >= 4 ? 4 : 2;  // every tile as strips
+    q = 0;
+    r = tiles;
+  } else if (r > 0) {
+    double best = 1.0;
+    for (int s : {2, 4}) {
+      const double cost = (double)((r * s + G - 1) / G) / s;
+      if (cost < best - 1e-9) {
+        best = cost;
+        split = s;
+      }
+    }
+  }
+  const long long main_tiles = split == 1 ? tiles : q * G;
+  cudaError_t e = cudaSuccess;
+  if (main_tiles > 0)
+    e = vec2 ? launch_split<2>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream)
+             : launch_split<1>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream);
+  if (e != cudaSuccess || split == 1) return e;
+  const unsigned grid = (unsigned)((tiles - main_tiles) * split);
+  return vec2 ? launch_split<2>(split, grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles, stream)
+              : launch_split<1>(split, grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
+                                stream);
 }
 
 }  // namespace myd

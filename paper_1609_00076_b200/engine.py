@@ -124,10 +124,11 @@ def check_conformal(a, b, c) -> tuple[int, int, int]:
     return a.m, b.n, a.n
 
 
-def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False) -> int:
+def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, strips: int = 0) -> int:
     f = _capi.EXACT if exact else 0
     f |= _capi.FORCE_TILED if force_tiled else 0
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
+    f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4}[strips]
     return f
 
 
@@ -205,11 +206,12 @@ def my_dgemm(m: int, n: int, k: int, A: np.ndarray, lda: int, B: np.ndarray, ldb
 
 def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int, ldc: int,
                  stream: int = 0, exact: bool = False, force_tiled: bool = False,
-                 force_vec1: bool = False) -> None:
-    """Raw device-pointer call (asynchronous on `stream`)."""
+                 force_vec1: bool = False, strips: int = 0) -> None:
+    """Raw device-pointer call (asynchronous on `stream`).  `strips` (2 or 4)
+    forces every tile through the narrow-strip kernels (tests)."""
     lib = _capi.load()
     _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
-                                _flags(exact, force_tiled, force_vec1) | _capi.DEVICE_PTRS,
+                                _flags(exact, force_tiled, force_vec1, strips) | _capi.DEVICE_PTRS,
                                 ctypes.c_void_p(stream)))
 
 
