@@ -298,3 +298,26 @@ def test_reference_registry_gate_admits_b200(torch_cuda):
     got = eng(a, b, gf.matrix.copy_matrix(c))
     rep = gf.matrix.max_abs_diff(got, want, gf.kernels.tolerance(83, 1.0, 1.0))
     assert rep.first_bad_i is None
+
+
+def test_reference_cli_verify_and_bench_with_b200(torch_cuda):
+    """The reference's own CLI (cmd_verify / cmd_bench, cli.py:83-107) drives
+    the engine through the registry: exit code 0, every shape PASS."""
+    import os
+    import subprocess
+    import sys
+
+    from conftest import REPO, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref (the reference package) not built")
+    tool = os.path.join(REPO, "tools", "run_gemmforge_b200.py")
+    r = subprocess.run([sys.executable, tool, "verify", "--alg", "b200"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
+    r = subprocess.run([sys.executable, tool, "bench", "--alg", "b200", "--min", "128", "--max", "256",
+                        "--step", "128", "--check", "--format", "csv", "--reps", "1"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert ",b200," in r.stdout
