@@ -1,7 +1,5 @@
 // dgemm_aux.cu -- the other kernels on the my_dgemm path (sm_100a):
 //   * dgemm_exact   bitwise twin of the reference oracle (verification mode)
-//   * gemv_n1       n == 1   (cfg 3c)  HBM-bound, deterministic in-CTA split-K
-//   * gemv_m1       m == 1   (cfg 3b)  HBM-bound, one warp per column
 //   * fill_random   splitmix64-v1 operand generator, bit-exact with the reference
 //   * max_abs_diff  device-side parity metric
 #include <algorithm>
@@ -88,117 +86,6 @@ cudaError_t launch_dgemm_exact(int M, int N, int K, const double *A, int64_t lda
     dgemm_exact_kernel<<<dim3(gx, gy), THREADS, 0, stream>>>(M, N, K, A, lda, B, ldb, C, ldc);
     count_launch();
   }
-  return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// n == 1: C(:,0) += A * b.  A is column-major (rows contiguous), b = B(:,0)
-// contiguous.  A CTA owns 32 rows; its 16 warps take interleaved k-slices
-// (warp w: p = w, w+16, ...), each lane one row, so every warp load is one
-// coalesced 256-byte column segment.  Partial sums meet in shared memory and
-// are added in fixed warp order: deterministic, no workspace, one launch.
-// Algorithmic bytes 8*(mk + k + 2m); HBM-bound (cfg 3c).
-// ---------------------------------------------------------------------------
-namespace gemv {
-constexpr int ROWS = 32, WARPS = 16, UNROLL = 8;
-}
-
-__global__ void __launch_bounds__(gemv::ROWS *gemv::WARPS)
-    gemv_n1_kernel(int M, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ b,
-                   double *__restrict__ C) {
-  using namespace gemv;
-  __shared__ double part[WARPS][ROWS];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int row = blockIdx.x * ROWS + lane;
-  double acc = 0.0;
-  if (row < M) {
-    const double *a = A + row;
-    int p = warp;
-    for (; p + (UNROLL - 1) * WARPS < K; p += UNROLL * WARPS) {
-      double av[UNROLL], bv[UNROLL];
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        av[u] = __ldcs(a + (int64_t)(p + u * WARPS) * lda);
-        bv[u] = __ldg(b + p + u * WARPS);
-      }
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) acc = fma(av[u], bv[u], acc);
-    }
-    for (; p < K; p += WARPS) acc = fma(__ldcs(a + (int64_t)p * lda), __ldg(b + p), acc);
-  }
-  part[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && row < M) {
-    double s = C[row];
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) s += part[w][lane];
-    C[row] = s;
-  }
-}
-
-// m == 1: C(0,j) += sum_p A(0,p) B(p,j).  The A row (stride lda) is staged
-// in shared memory chunk by chunk; each warp owns COLS columns and streams
-// them with coalesced 256-byte loads; a fixed xor-shuffle tree reduces.
-namespace gemv {
-constexpr int M1_WARPS = 8, M1_COLS = 2, M1_CHUNK = 4096;
-}
-
-__global__ void __launch_bounds__(gemv::M1_WARPS * 32)
-    gemv_m1_kernel(int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
-                   double *__restrict__ C, int64_t ldc) {
-  using namespace gemv;
-  __shared__ double arow[M1_CHUNK];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t j0 = ((int64_t)blockIdx.x * M1_WARPS + warp) * M1_COLS;
-  double acc[M1_COLS];
-#pragma unroll
-  for (int c = 0; c < M1_COLS; ++c) acc[c] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += M1_CHUNK) {
-    const int kv = min(M1_CHUNK, K - k0);
-    __syncthreads();
-    for (int p = threadIdx.x; p < kv; p += blockDim.x) arow[p] = A[(int64_t)(k0 + p) * lda];
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < M1_COLS; ++c) {
-      const int64_t j = j0 + c;
-      if (j >= N) break;
-      const double *bc = B + j * ldb + k0;
-      int p = lane;
-      for (; p + 96 < kv; p += 128) {
-        const double b0 = __ldcs(bc + p), b1 = __ldcs(bc + p + 32), b2 = __ldcs(bc + p + 64), b3 = __ldcs(bc + p + 96);
-        acc[c] = fma(arow[p], b0, acc[c]);
-        acc[c] = fma(arow[p + 32], b1, acc[c]);
-        acc[c] = fma(arow[p + 64], b2, acc[c]);
-        acc[c] = fma(arow[p + 96], b3, acc[c]);
-      }
-      for (; p < kv; p += 32) acc[c] = fma(arow[p], __ldcs(bc + p), acc[c]);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < M1_COLS; ++c) {
-    double v = acc[c];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    const int64_t j = j0 + c;
-    if (lane == 0 && j < N) C[j * ldc] = C[j * ldc] + v;
-  }
-}
-
-cudaError_t launch_gemv_n1(int M, int K, const double *A, int64_t lda, const double *b, double *C,
-                           cudaStream_t stream) {
-  using namespace gemv;
-  gemv_n1_kernel<<<(M + ROWS - 1) / ROWS, ROWS * WARPS, 0, stream>>>(M, K, A, lda, b, C);
-  count_launch();
-  return cudaGetLastError();
-}
-
-cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
-                           int64_t ldc, cudaStream_t stream) {
-  using namespace gemv;
-  const int64_t per_cta = (int64_t)M1_WARPS * M1_COLS;
-  const int64_t grid = (N + per_cta - 1) / per_cta;
-  gemv_m1_kernel<<<(unsigned)grid, M1_WARPS * 32, 0, stream>>>(N, K, A, lda, B, ldb, C, ldc);
-  count_launch();
   return cudaGetLastError();
 }
 
