@@ -5,8 +5,7 @@
 // matrix.py:50-53).  The host-pointer path stages operands through cached
 // device workspace with pitched copies (width m*8, pitch ld*8), so padding
 // rows are never read or written and nothing past (n-1)*ld+m is touched
-// (matrix.py:5-6,42-45,58-61).  It pipelines column panels of B and C:
-// H2D(panel p+1) and D2H(panel p-1) overlap the GEMM of panel p.
+// (matrix.py:5-6,42-45,58-61).  Large problems are pipelined (host_path).
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -105,7 +104,7 @@ struct Workspace {
   double *dA = nullptr, *dB = nullptr, *dC = nullptr;
   size_t capA = 0, capB = 0, capC = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_done;
+  std::vector<cudaEvent_t> ev_in, ev_done, ev_out;
 };
 
 std::mutex g_ws_mutex;
@@ -129,11 +128,13 @@ cudaError_t ensure_streams(Workspace &w, size_t panels) {
     if ((e = cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
   }
   while (w.ev_in.size() < panels) {
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, c;
     if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c, cudaEventDisableTiming)) != cudaSuccess) return e;
     w.ev_in.push_back(a);
     w.ev_done.push_back(b);
+    w.ev_out.push_back(c);
   }
   return cudaSuccess;
 }
@@ -150,43 +151,76 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   // Device copies use even leading dimensions so every column starts 16-byte
   // aligned and the 16-byte staging path applies whatever the host ld was.
   const int64_t dlda = (m + 1) & ~1LL, dldb = (k + 1) & ~1LL, dldc = (m + 1) & ~1LL;
-  // Panel width: 1 panel for small problems, else ~8 panels of >=512 columns,
-  // multiples of the 128-column CTA tile.
-  int64_t panel = n;
+  // Schedule (host path, large problems).  Measured on the B200 box: 55 GB/s
+  // H2D and 57 GB/s D2H over PCIe 5, but only ~34 GB/s in total when both
+  // directions run at once, so uploads go first and downloads are deferred
+  // until every upload is queued; the GEMM overlaps both.  Panel 0 is
+  // computed in k-chunks as A arrives (chunks are multiples of 16, so the
+  // result is bitwise the unchunked one); panels 1.. run whole as their B and
+  // C land; each panel's C goes down as soon as it is final.
   const double flops = 2.0 * m * (double)n * k;
-  if (flops > 4e9 && n >= 1024 && m > 1 && n > 1) {
+  const bool pipelined = flops > 4e9 && n >= 1024 && m > 1 && n > 1;
+  int64_t panel = n;
+  if (pipelined) {
     panel = ((n / 8 + 127) / 128) * 128;
     if (panel < 512) panel = 512;
   }
   const size_t panels = (size_t)((n + panel - 1) / panel);
-  if ((e = ensure_streams(w, panels)) != cudaSuccess) return cuda_fail(e, "stream setup");
+  int64_t kchunk = k;
+  if (pipelined && k >= 256) kchunk = (((k + 7) / 8) + 15) / 16 * 16;
+  const size_t kchunks = (size_t)((k + kchunk - 1) / kchunk);
+  if ((e = ensure_streams(w, std::max(panels, kchunks) + 1)) != cudaSuccess) return cuda_fail(e, "stream setup");
   if ((e = grow(&w.dA, &w.capA, (size_t)dlda * k * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(A)");
   if ((e = grow(&w.dB, &w.capB, (size_t)dldb * n * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(B)");
   if ((e = grow(&w.dC, &w.capC, (size_t)dldc * n * 8)) != cudaSuccess) return cuda_fail(e, "cudaMalloc(C)");
 
-  // A first (every panel needs it), then B/C panels in order on the copy stream.
-  e = cudaMemcpy2DAsync(w.dA, dlda * 8, A, (size_t)lda * 8, (size_t)m * 8, k, cudaMemcpyHostToDevice, w.s_h2d);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D A");
-  for (size_t p = 0; p < panels; ++p) {
-    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
-    e = cudaMemcpy2DAsync(w.dB + j0 * dldb, dldb * 8, B + j0 * ldb, (size_t)ldb * 8, (size_t)k * 8, nc,
-                          cudaMemcpyHostToDevice, w.s_h2d);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D B");
-    e = cudaMemcpy2DAsync(w.dC + j0 * dldc, dldc * 8, C + j0 * ldc, (size_t)ldc * 8, (size_t)m * 8, nc,
-                          cudaMemcpyHostToDevice, w.s_h2d);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D C");
-    cudaEventRecord(w.ev_in[p], w.s_h2d);
+  auto h2d = [&](double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols) {
+    return cudaMemcpy2DAsync(dst, dpitch * 8, src, (size_t)spitch * 8, (size_t)rows * 8, cols,
+                             cudaMemcpyHostToDevice, w.s_h2d);
+  };
+  const int64_t nc0 = std::min<int64_t>(panel, n);
+  // uploads: C_0, then (A chunk, B_0 chunk) pairs, then (B_p, C_p)
+  if ((e = h2d(w.dC, dldc, C, ldc, m, nc0)) != cudaSuccess) return cuda_fail(e, "H2D C");
+  for (size_t c = 0; c < kchunks; ++c) {
+    const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
+    if ((e = h2d(w.dA + p0 * dlda, dlda, A + p0 * lda, lda, m, kl)) != cudaSuccess) return cuda_fail(e, "H2D A");
+    if ((e = h2d(w.dB + p0, dldb, B + p0, ldb, kl, nc0)) != cudaSuccess) return cuda_fail(e, "H2D B");
+    cudaEventRecord(w.ev_in[c], w.s_h2d);
   }
-  for (size_t p = 0; p < panels; ++p) {
+  for (size_t p = 1; p < panels; ++p) {
     const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
-    cudaStreamWaitEvent(w.s_comp, w.ev_in[p], 0);
+    if ((e = h2d(w.dB + j0 * dldb, dldb, B + j0 * ldb, ldb, k, nc)) != cudaSuccess) return cuda_fail(e, "H2D B");
+    if ((e = h2d(w.dC + j0 * dldc, dldc, C + j0 * ldc, ldc, m, nc)) != cudaSuccess) return cuda_fail(e, "H2D C");
+    cudaEventRecord(w.ev_done[p], w.s_h2d);  // reused below as the panel's "inputs landed" event
+  }
+  cudaEvent_t all_in = w.ev_in[kchunks];  // every upload done: downloads may start
+  cudaEventRecord(all_in, w.s_h2d);
+
+  // compute: panel 0 by k-chunks, then whole panels
+  for (size_t c = 0; c < kchunks; ++c) {
+    const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
+    cudaStreamWaitEvent(w.s_comp, w.ev_in[c], 0);
+    e = dispatch(m, (int)nc0, (int)kl, w.dA + p0 * dlda, dlda, w.dB + p0, dldb, w.dC, dldc, w.s_comp, flags);
+    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  }
+  auto d2h = [&](int64_t j0, int64_t nc) {
+    return cudaMemcpy2DAsync(C + j0 * ldc, (size_t)ldc * 8, w.dC + j0 * dldc, dldc * 8, (size_t)m * 8, nc,
+                             cudaMemcpyDeviceToHost, w.s_d2h);
+  };
+  std::vector<cudaEvent_t> &done = w.ev_out;
+  cudaEventRecord(done[0], w.s_comp);
+  for (size_t p = 1; p < panels; ++p) {
+    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
+    cudaStreamWaitEvent(w.s_comp, w.ev_done[p], 0);
     e = dispatch(m, (int)nc, k, w.dA, dlda, w.dB + j0 * dldb, dldb, w.dC + j0 * dldc, dldc, w.s_comp, flags);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-    cudaEventRecord(w.ev_done[p], w.s_comp);
-    cudaStreamWaitEvent(w.s_d2h, w.ev_done[p], 0);
-    e = cudaMemcpy2DAsync(C + j0 * ldc, (size_t)ldc * 8, w.dC + j0 * dldc, dldc * 8, (size_t)m * 8, nc,
-                          cudaMemcpyDeviceToHost, w.s_d2h);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H C");
+    cudaEventRecord(done[p], w.s_comp);
+  }
+  cudaStreamWaitEvent(w.s_d2h, all_in, 0);
+  for (size_t p = 0; p < panels; ++p) {
+    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
+    cudaStreamWaitEvent(w.s_d2h, done[p], 0);
+    if ((e = d2h(j0, nc)) != cudaSuccess) return cuda_fail(e, "D2H C");
   }
   e = cudaStreamSynchronize(w.s_d2h);
   if (e != cudaSuccess) return cuda_fail(e, "synchronize");

@@ -7,6 +7,7 @@
 // shapes with the same five-loop code as every other shape
 // (goto.py:187-239); on the GPU they are bandwidth problems, not DMMA ones.
 #include <algorithm>
+#include <atomic>
 
 #include "common.cuh"
 
@@ -143,12 +144,16 @@ cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const dou
   const unsigned grid = (unsigned)std::min<int64_t>(want, sm_count_skinny());
   const size_t smem = (size_t)K * 8;
   if (smem <= 160 * 1024) {
-    static bool attr = false;  // idempotent; a race only repeats the call
-    if (!attr) {
+    // per-device function attribute, set once per device (a race only repeats it)
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
       cudaError_t e = cudaFuncSetAttribute(gemv_m1_kernel<TEAM, MYD_M1_UNROLL, true>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr_done.fetch_or(bit, std::memory_order_release);
     }
     gemv_m1_kernel<TEAM, MYD_M1_UNROLL, true><<<grid, threads, smem, stream>>>(N, K, A, lda, B, ldb, C, ldc);
   } else {

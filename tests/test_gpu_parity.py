@@ -321,3 +321,21 @@ def test_reference_cli_verify_and_bench_with_b200(torch_cuda):
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert ",b200," in r.stdout
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (2048, 2048, 2048, 2048, 2048, 2048),   # pipelined host path: 4 panels, 8 k-chunks
+    (1500, 3000, 1000, 1507, 1003, 1501),   # odd host lds, pipelined
+])
+def test_host_path_pipeline_bitwise_equals_device_path(torch_cuda, m, n, k, lda, ldb, ldc):
+    """The host-pointer path (panel pipeline, k-chunked first panel) returns
+    bitwise what the device-pointer path computes, and never writes padding."""
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, lda, ldb, ldc, canary=-777.25)
+    got = engine.my_dgemm(m, n, k, a, lda, b, ldb, c.copy(), ldc)
+    da = torch_cuda.from_numpy(a).cuda()
+    db = torch_cuda.from_numpy(b).cuda()
+    dc = torch_cuda.from_numpy(c).cuda()
+    run_dev(torch_cuda, m, n, k, da, lda, db, ldb, dc, ldc)
+    dev = dc.cpu().numpy()
+    assert np.array_equal(oracle.valid_region(got, m, n, ldc), oracle.valid_region(dev, m, n, ldc))
+    assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
