@@ -154,18 +154,21 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   // Schedule (host path, large problems).  Measured on the B200 box: 55 GB/s
   // H2D and 57 GB/s D2H over PCIe 5, but only ~34 GB/s in total when both
   // directions run at once, so uploads go first and downloads are deferred
-  // until every upload is queued; the GEMM overlaps both.  Panel 0 is
-  // computed in k-chunks as A arrives (chunks are multiples of 16, so the
-  // result is bitwise the unchunked one); panels 1.. run whole as their B and
-  // C land; each panel's C goes down as soon as it is final.
+  // until every upload is queued; the GEMM overlaps both.  A first column
+  // group (half of C) is computed in k-chunks as A arrives, so the GEMM runs
+  // at full width while A is still uploading (chunks are multiples of 16:
+  // bitwise the unchunked result); the remaining panels run whole as their
+  // B and C land.  (tools/e2e_schedule_sim.py models the alternatives.)
   const double flops = 2.0 * m * (double)n * k;
   const bool pipelined = flops > 4e9 && n >= 1024 && m > 1 && n > 1;
-  int64_t panel = n;
+  int64_t nc0 = n, panel = n;
   if (pipelined) {
-    panel = ((n / 8 + 127) / 128) * 128;
-    if (panel < 512) panel = 512;
+    nc0 = std::max<int64_t>(128, (n / 2) / 128 * 128);
+    panel = std::max<int64_t>(512, ((n / 8 + 127) / 128) * 128);
   }
-  const size_t panels = (size_t)((n + panel - 1) / panel);
+  const size_t panels = 1 + (size_t)((n - nc0 + panel - 1) / panel);  // group 0 + whole panels
+  auto panel_j0 = [&](size_t p) -> int64_t { return p == 0 ? 0 : nc0 + (int64_t)(p - 1) * panel; };
+  auto panel_nc = [&](size_t p) -> int64_t { return p == 0 ? nc0 : std::min<int64_t>(panel, n - panel_j0(p)); };
   int64_t kchunk = k;
   if (pipelined && k >= 256) kchunk = (((k + 7) / 8) + 15) / 16 * 16;
   const size_t kchunks = (size_t)((k + kchunk - 1) / kchunk);
@@ -178,8 +181,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
     return cudaMemcpy2DAsync(dst, dpitch * 8, src, (size_t)spitch * 8, (size_t)rows * 8, cols,
                              cudaMemcpyHostToDevice, w.s_h2d);
   };
-  const int64_t nc0 = std::min<int64_t>(panel, n);
-  // uploads: C_0, then (A chunk, B_0 chunk) pairs, then (B_p, C_p)
+  // uploads: C of group 0, then (A chunk, B chunk of group 0) pairs, then (B_p, C_p)
   if ((e = h2d(w.dC, dldc, C, ldc, m, nc0)) != cudaSuccess) return cuda_fail(e, "H2D C");
   for (size_t c = 0; c < kchunks; ++c) {
     const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
@@ -188,7 +190,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
     cudaEventRecord(w.ev_in[c], w.s_h2d);
   }
   for (size_t p = 1; p < panels; ++p) {
-    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
+    const int64_t j0 = panel_j0(p), nc = panel_nc(p);
     if ((e = h2d(w.dB + j0 * dldb, dldb, B + j0 * ldb, ldb, k, nc)) != cudaSuccess) return cuda_fail(e, "H2D B");
     if ((e = h2d(w.dC + j0 * dldc, dldc, C + j0 * ldc, ldc, m, nc)) != cudaSuccess) return cuda_fail(e, "H2D C");
     cudaEventRecord(w.ev_done[p], w.s_h2d);  // reused below as the panel's "inputs landed" event
@@ -196,7 +198,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   cudaEvent_t all_in = w.ev_in[kchunks];  // every upload done: downloads may start
   cudaEventRecord(all_in, w.s_h2d);
 
-  // compute: panel 0 by k-chunks, then whole panels
+  // compute: group 0 by k-chunks, then whole panels
   for (size_t c = 0; c < kchunks; ++c) {
     const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
     cudaStreamWaitEvent(w.s_comp, w.ev_in[c], 0);
@@ -210,7 +212,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   std::vector<cudaEvent_t> &done = w.ev_out;
   cudaEventRecord(done[0], w.s_comp);
   for (size_t p = 1; p < panels; ++p) {
-    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
+    const int64_t j0 = panel_j0(p), nc = panel_nc(p);
     cudaStreamWaitEvent(w.s_comp, w.ev_done[p], 0);
     e = dispatch(m, (int)nc, k, w.dA, dlda, w.dB + j0 * dldb, dldb, w.dC + j0 * dldc, dldc, w.s_comp, flags);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
@@ -218,7 +220,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   }
   cudaStreamWaitEvent(w.s_d2h, all_in, 0);
   for (size_t p = 0; p < panels; ++p) {
-    const int64_t j0 = (int64_t)p * panel, nc = std::min<int64_t>(panel, n - j0);
+    const int64_t j0 = panel_j0(p), nc = panel_nc(p);
     cudaStreamWaitEvent(w.s_d2h, done[p], 0);
     if ((e = d2h(j0, nc)) != cudaSuccess) return cuda_fail(e, "D2H C");
   }
