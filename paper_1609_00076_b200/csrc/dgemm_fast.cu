@@ -96,7 +96,8 @@ constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier
 template <int VEC, int BN>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
-                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0) {
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                      int units) {
   using namespace fast;
   constexpr int SPLIT = TILE_N / BN;
   constexpr int WARPS_N = BN / WN;
@@ -112,17 +113,17 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   __shared__ __align__(8) uint64_t full_bar[STAGES];
   __shared__ __align__(8) uint64_t empty_bar[STAGES];
 
-  // Grouped raster over full tiles: GROUP_M tile-rows per band, column-major
-  // inside a band.  Strip launches cut tile (tile0 + bid/SPLIT) into SPLIT
-  // column strips.
-  const int tile = tile0 + (int)(blockIdx.x / SPLIT);
-  const int strip = (int)(blockIdx.x % SPLIT);
-  const int band = GROUP_M * tiles_n;
-  const int first_m = (tile / band) * GROUP_M;
-  const int gm = min(tiles_m - first_m, GROUP_M);
-  const int tm = first_m + (tile % band) % gm;
-  const int tn = (tile % band) / gm;
-  const int m0 = tm * BM, n0 = tn * TILE_N + strip * BN;
+  // Work unit u (persistent CTA b takes u = b, b + gridDim.x, ...): full
+  // tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows per band,
+  // column-major inside a band), column strip u % SPLIT of it.
+  auto unit_origin = [&](int u, int &m0, int &n0) {
+    const int tile = tile0 + u / SPLIT;
+    const int band = GROUP_M * tiles_n;
+    const int first_m = (tile / band) * GROUP_M;
+    const int gm = min(tiles_m - first_m, GROUP_M);
+    m0 = (first_m + (tile % band) % gm) * BM;
+    n0 = ((tile % band) / gm) * TILE_N + (u % SPLIT) * BN;
+  };
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -142,80 +143,101 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     // ================= producers: pack_a / pack_b equivalent =================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
-    // Interior tiles with 16-byte aligned operands use the bulk-copy (TMA)
-    // engine straight into the padded slab layout, with no LSU traffic.
-    // Edge tiles and a ragged last slab use zero-filling LDGSTS.
-    const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
-    for (int kt = 0; kt < KT; ++kt) {
-      const int slot = kt % STAGES;
-      if (kt >= STAGES) {
-        PROF_T0();
-        mbar_wait(&empty_bar[slot], ((kt / STAGES) - 1) & 1);
-        if (lane == 0) {
-          PROF_ADD(2, clock64() - _pt0);
-          PROF_ADD(3, 1);
+    uint32_t g = 0;  // slabs staged by this CTA so far (ring position)
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int m0, n0;
+      unit_origin(u, m0, n0);
+      // Warm L2 with the C tile of this CTA's next unit: its consumers load
+      // it at the start of that unit, right when the ring is already full.
+      if (u + (int)gridDim.x < units) {
+        int pm0, pn0;
+        unit_origin(u + gridDim.x, pm0, pn0);
+        const int rows = min(BM, M - pm0);
+        if (pw * RW + (lane % RW) < BN && lane < RW) {
+          const int col = pn0 + pw * RW + lane;
+          if (col < N && rows > 0) {
+            const double *c0 = C + (int64_t)col * ldc + pm0;
+            for (int off = 0; off < rows; off += 16)
+              asm volatile("prefetch.global.L2 [%0];\n" ::"l"(c0 + off));
+            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(c0 + rows - 1));
+          }
         }
       }
-      const int kbase = kt * BK;
-      double *as = As + slot * A_STAGE;
-      double *bs = Bs + slot * B_STAGE;
-      if (interior && kbase + BK <= K) {
-        constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
-        constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
-        if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
+      // Interior units with 16-byte aligned operands use the bulk-copy (TMA)
+      // engine straight into the padded slab layout, with no LSU traffic.
+      // Edge units and a ragged last slab use zero-filling LDGSTS.
+      const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
+      for (int kt = 0; kt < KT; ++kt, ++g) {
+        const int slot = g % STAGES;
+        if (g >= STAGES) {
+          PROF_T0();
+          mbar_wait(&empty_bar[slot], ((g / STAGES) - 1) & 1);
+          if (lane == 0) {
+            PROF_ADD(2, clock64() - _pt0);
+            PROF_ADD(3, 1);
+          }
+        }
+        const int kbase = kt * BK;
+        double *as = As + slot * A_STAGE;
+        double *bs = Bs + slot * B_STAGE;
+        if (interior && kbase + BK <= K) {
+          constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
+          constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
+          if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
+          __syncwarp();
+          if (lane < A_ROWS) {
+            const int kk = pw * A_ROWS + lane;
+            bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
+          }
+          if (lane < RW) {
+            const int nn = pw * RW + lane;
+            bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+          }
+          continue;
+        }
+        // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
+        // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
+#pragma unroll
+        for (int i = 0; i < BK * BM / (VEC * 32 * PRODUCER_WARPS); ++i) {
+          const int e = ((pw * 32 + lane) + i * 32 * PRODUCER_WARPS) * VEC;
+          const int kk = e / BM, mm = e % BM;
+          const int gk = kbase + kk, gmr = m0 + mm;
+          int bytes = 0;
+          const double *src = A;
+          if (gk < K && gmr < M) {
+            bytes = min(VEC, M - gmr) * 8;
+            src = A + (int64_t)gk * lda + gmr;
+          }
+          cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
+        }
+        // B slab [BN][BK], k contiguous: producer pw owns rows [RW*pw, RW*pw+RW).
+        // VEC=2: a quarter-warp writes 4 rows x 2 chunks (conflict-free at BP).
+#pragma unroll
+        for (int i = 0; i < RW * BK / (VEC * 32); ++i) {
+          const int idx = i * 32 + lane;
+          int nn, kk;
+          if constexpr (VEC == 2) {
+            nn = pw * RW + (idx >> 1) % RW;
+            kk = 2 * (((idx >> 1) / RW) * 2 + (idx & 1));
+          } else {
+            nn = pw * RW + (idx >> 2) % RW;
+            kk = ((idx >> 2) / RW) * 4 + (idx & 3);
+          }
+          const int gk = kbase + kk, gn = n0 + nn;
+          int bytes = 0;
+          const double *src = B;
+          if (gn < N && gk < K) {
+            bytes = min(VEC, K - gk) * 8;
+            src = B + (int64_t)gn * ldb + gk;
+          }
+          cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
+        }
+        // full_bar counts one arrival per producer warp; each lane's copies are
+        // tracked by its own pending +1/-1 (cp.async.mbarrier.arrive).
+        cp_async_mbar_arrive_inc(&full_bar[slot]);
         __syncwarp();
-        if (lane < A_ROWS) {
-          const int kk = pw * A_ROWS + lane;
-          bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
-        }
-        if (lane < RW) {
-          const int nn = pw * RW + lane;
-          bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
-        }
-        continue;
+        if (lane == 0) mbar_arrive(&full_bar[slot]);
       }
-      // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
-      // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
-#pragma unroll
-      for (int i = 0; i < BK * BM / (VEC * 32 * PRODUCER_WARPS); ++i) {
-        const int e = ((pw * 32 + lane) + i * 32 * PRODUCER_WARPS) * VEC;
-        const int kk = e / BM, mm = e % BM;
-        const int gk = kbase + kk, gmr = m0 + mm;
-        int bytes = 0;
-        const double *src = A;
-        if (gk < K && gmr < M) {
-          bytes = min(VEC, M - gmr) * 8;
-          src = A + (int64_t)gk * lda + gmr;
-        }
-        cp_async<VEC * 8>(as + kk * AP + mm, src, bytes);
-      }
-      // B slab [BN][BK], k contiguous: producer pw owns rows [RW*pw, RW*pw+RW).
-      // VEC=2: a quarter-warp writes 4 rows x 2 chunks (conflict-free at BP).
-#pragma unroll
-      for (int i = 0; i < RW * BK / (VEC * 32); ++i) {
-        const int idx = i * 32 + lane;
-        int nn, kk;
-        if constexpr (VEC == 2) {
-          nn = pw * RW + (idx >> 1) % RW;
-          kk = 2 * (((idx >> 1) / RW) * 2 + (idx & 1));
-        } else {
-          nn = pw * RW + (idx >> 2) % RW;
-          kk = ((idx >> 2) / RW) * 4 + (idx & 3);
-        }
-        const int gk = kbase + kk, gn = n0 + nn;
-        int bytes = 0;
-        const double *src = B;
-        if (gn < N && gk < K) {
-          bytes = min(VEC, K - gk) * 8;
-          src = B + (int64_t)gn * ldb + gk;
-        }
-        cp_async<VEC * 8>(bs + nn * BP + kk, src, bytes);
-      }
-      // full_bar counts one arrival per producer warp; each lane's copies are
-      // tracked by its own pending +1/-1 (cp.async.mbarrier.arrive).
-      cp_async_mbar_arrive_inc(&full_bar[slot]);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full_bar[slot]);
     }
     cp_async_wait<0>();
     return;
@@ -225,19 +247,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // ================= consumers: loops 2/1 + micro-kernel =================
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int r = lane >> 2, q = lane & 3;
-  double acc[FM][FN][2];
-  const int row0 = m0 + wm * WM + r;
-  const int col0 = n0 + wn * WN + 2 * q;
-#pragma unroll
-  for (int i = 0; i < FM; ++i)
-#pragma unroll
-    for (int j = 0; j < FN; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int row = row0 + i * 8, col = col0 + j * 8 + e;
-        acc[i][j][e] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
-      }
-
   const int a_off = q * AP + wm * WM + r;    // + kk*4*AP + i*8
   const int b_off = (wn * WN + r) * BP + q;  // + j*8*BP + kk*4
   double fa[2][FM], fb[2][FN];
@@ -250,67 +259,88 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     for (int j = 0; j < FN; ++j) fb[buf][j] = bs[j * 8 * BP];
   };
 
-#ifdef MYD_FAST_PROFILE
-  long long loop_t0 = clock64();
-#endif
-  {
-    PROF_T0();
-    mbar_wait(&full_bar[0], 0);
-    if (lane == 0) PROF_ADD(4, clock64() - _pt0);
-  }
-  load_frags(0, 0, 0);
-  for (int kt = 0; kt < KT; ++kt) {
-    const int slot = kt % STAGES;
-    const int nslot = (kt + 1) % STAGES;
-    const uint32_t nparity = ((kt + 1) / STAGES) & 1;
-    bool next_ready = true;
+  uint32_t g = 0;  // ring position of this unit's first slab
+  for (int u = blockIdx.x; u < units; u += gridDim.x, g += KT) {
+    int m0, n0;
+    unit_origin(u, m0, n0);
+    double acc[FM][FN][2];
+    const int row0 = m0 + wm * WM + r;
+    const int col0 = n0 + wn * WN + 2 * q;
 #pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-      const int cur = kk & 1;
-      // Probe the next slab's barrier early; its latency hides behind DMMAs.
-      if (kk == PROBE_STEP && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
-      if (kk + 1 < KSTEPS) {
-        load_frags(cur ^ 1, slot, kk + 1);
-      } else if (kt + 1 < KT) {
-        if (!next_ready) {
-          PROF_T0();
-          mbar_wait(&full_bar[nslot], nparity);
-          if (lane == 0) {
-            PROF_ADD(0, clock64() - _pt0);
-            PROF_ADD(1, 1);
-          }
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = row0 + i * 8, col = col0 + j * 8 + e;
+          acc[i][j][e] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
         }
-        load_frags(cur ^ 1, nslot, 0);
-      }
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fa[cur][i], fb[cur][j]);
-    }
-    // every fragment of this slab has been consumed by an issued DMMA
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar[slot]);
-  }
 
 #ifdef MYD_FAST_PROFILE
-  if (lane == 0) PROF_ADD(5, clock64() - loop_t0);
+    long long loop_t0 = clock64();
 #endif
-  // ---- epilogue: valid region only (padding rows never touched) ----
+    {
+      PROF_T0();
+      mbar_wait(&full_bar[g % STAGES], (g / STAGES) & 1);
+      if (lane == 0) PROF_ADD(4, clock64() - _pt0);
+    }
+    load_frags(0, g % STAGES, 0);
+    for (int kt = 0; kt < KT; ++kt) {
+      const uint32_t gs = g + kt;
+      const int slot = gs % STAGES;
+      const int nslot = (gs + 1) % STAGES;
+      const uint32_t nparity = ((gs + 1) / STAGES) & 1;
+      bool next_ready = true;
 #pragma unroll
-  for (int i = 0; i < FM; ++i)
+      for (int kk = 0; kk < KSTEPS; ++kk) {
+        const int cur = kk & 1;
+        // Probe the next slab's barrier early; its latency hides behind DMMAs.
+        if (kk == PROBE_STEP && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
+        if (kk + 1 < KSTEPS) {
+          load_frags(cur ^ 1, slot, kk + 1);
+        } else if (kt + 1 < KT) {
+          if (!next_ready) {
+            PROF_T0();
+            mbar_wait(&full_bar[nslot], nparity);
+            if (lane == 0) {
+              PROF_ADD(0, clock64() - _pt0);
+              PROF_ADD(1, 1);
+            }
+          }
+          load_frags(cur ^ 1, nslot, 0);
+        }
 #pragma unroll
-    for (int j = 0; j < FN; ++j)
+        for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int row = row0 + i * 8, col = col0 + j * 8 + e;
-        if (row < M && col < N) C[(int64_t)col * ldc + row] = acc[i][j][e];
+          for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fa[cur][i], fb[cur][j]);
       }
+      // every fragment of this slab has been consumed by an issued DMMA
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    }
+
+#ifdef MYD_FAST_PROFILE
+    if (lane == 0) PROF_ADD(5, clock64() - loop_t0);
+#endif
+    // ---- epilogue: valid region only (padding rows never touched) ----
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int row = row0 + i * 8, col = col0 + j * 8 + e;
+          if (row < M && col < N) C[(int64_t)col * ldc + row] = acc[i][j][e];
+        }
+  }
 }
 
 namespace {
 
+int sm_count();
+
 template <int VEC, int BN>
-cudaError_t launch_one(unsigned grid, int M, int N, int K, const double *A, int64_t lda, const double *B,
+cudaError_t launch_one(unsigned units, int M, int N, int K, const double *A, int64_t lda, const double *B,
                        int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, cudaStream_t st) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
@@ -325,20 +355,22 @@ cudaError_t launch_one(unsigned grid, int M, int N, int K, const double *A, int6
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
   }
+  // persistent: at most one CTA per SM, each walking units b, b+grid, ...
+  const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
   dgemm_fast_kernel<VEC, BN>
-      <<<grid, THREADS, SMEM_BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0);
+      <<<grid, THREADS, SMEM_BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int VEC>
-cudaError_t launch_split(int split, unsigned grid, int M, int N, int K, const double *A, int64_t lda,
+cudaError_t launch_split(int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                          cudaStream_t st) {
   switch (split) {
-    case 1: return launch_one<VEC, 128>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 2: return launch_one<VEC, 64>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    default: return launch_one<VEC, 32>(grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 1: return launch_one<VEC, 128>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 2: return launch_one<VEC, 64>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    default: return launch_one<VEC, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
   }
 }
 
