@@ -370,7 +370,7 @@ def run_b200_arm(args):
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                         "traffic": traffic, "kernel": "dgemm_fast_kernel<2>",
+                         "traffic": traffic, "kernel": "dgemm_fast_kernel<2,128> (+ <2,32> tail strips; one call = both launches)",
                          "peak_source": "nominal FP64 148SMx128flop/clkx1.965GHz (not in MEASURED_PEAKS.json); "
                                         f"DMMA microbench {FP64_PEAK_MEASURED}",
                          "launches_timed": len(kern_ms), "mean_launch_ms": round(mean_kernel_s * 1e3, 4)},
@@ -458,7 +458,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2_8192")
-    ap.add_argument("--k-chunk", type=int, default=1024)
+    ap.add_argument("--k-chunk", type=int, default=2048)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
