@@ -46,6 +46,7 @@ extern "C" {
 #define MY_DGEMM_FORCE_VEC1 0x8u  /* force 8-byte operand staging (odd-ld path) */
 #define MY_DGEMM_FORCE_STRIPS2 0x10u /* run every tile as two 128x64 strips (tests) */
 #define MY_DGEMM_FORCE_STRIPS4 0x20u /* run every tile as four 128x32 strips (tests) */
+#define MY_DGEMM_FORCE_UNITS8 0x40u  /* run every tile as eight 64x32 units (tests) */
 
 /*
  * The BASELINE.json north_star signature.  Replaces the reference's

@@ -21,6 +21,7 @@ FORCE_TILED = 0x4
 FORCE_VEC1 = 0x8
 FORCE_STRIPS2 = 0x10
 FORCE_STRIPS4 = 0x20
+FORCE_UNITS8 = 0x40
 
 # Every symbol the header declares, with (restype, argtypes).
 _P = ctypes.c_void_p

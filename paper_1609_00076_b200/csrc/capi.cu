@@ -94,7 +94,10 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     if (n == 1) return launch_gemv_n1(m, k, A, lda, B, C, st);
     if (m == 1) return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st);
   }
-  const int split = (flags & MY_DGEMM_FORCE_STRIPS4) ? 4 : ((flags & MY_DGEMM_FORCE_STRIPS2) ? 2 : 0);
+  const int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
+                    : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
+                    : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
+                                                       : 0;
   return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, (flags & MY_DGEMM_FORCE_VEC1) != 0, split);
 }
 
@@ -240,7 +243,7 @@ int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, 
   int v = validate(m, n, k, A, lda, B, ldb, C, ldc);
   if (v) return v;
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
-                         MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4;
+                         MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8;
   if (flags & ~known) return fail(-10, "unknown flag bits");
   if (flags & MY_DGEMM_DEVICE_PTRS) {
     cudaError_t e = dispatch(m, n, k, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, flags);

@@ -9,7 +9,7 @@
 //                         SM gets work (launch_dgemm_fast);
 //   loop 4 (pc)        -> the in-CTA K loop over BK=16 slabs;
 //   pack_a / pack_b    -> producer warps stage each A and B slab into a
-//                         STAGES-deep shared-memory ring: bulk copies by the
+//                         multi-stage shared-memory ring: bulk copies by the
 //                         TMA engine (cp.async.bulk, one per A k-row and per
 //                         B column segment) for interior tiles, zero-filling
 //                         cp.async (LDGSTS) at the edges; no pack pass touches
@@ -49,16 +49,17 @@ namespace fast {
 #ifndef MYD_FAST_BK
 #define MYD_FAST_BK 16
 #endif
-#ifndef MYD_FAST_STAGES
-#define MYD_FAST_STAGES 5
+#ifndef MYD_FAST_SMEM_KB
+#define MYD_FAST_SMEM_KB 200
 #endif
 #ifndef MYD_FAST_GROUP_M
 #define MYD_FAST_GROUP_M 8
 #endif
-constexpr int BM = 128;                  // CTA tile rows (m)
+constexpr int TILE_M = 128;              // full CTA tile rows (m); small-problem units are 64 high
 constexpr int TILE_N = 128;              // full CTA tile cols (n); strips are TILE_N / split wide
 constexpr int BK = MYD_FAST_BK;          // K slab per pipeline stage
-constexpr int STAGES = MYD_FAST_STAGES;  // ring depth
+constexpr int MAX_STAGES = 16;                        // ring depth cap (mbarrier arrays)
+constexpr int SMEM_BUDGET = MYD_FAST_SMEM_KB * 1024;  // ring bytes per CTA
 constexpr int CONSUMER_WARPS = 8;        // 2 per SM sub-partition
 constexpr int PRODUCER_WARPS = 4;        // one staging warp per sub-partition
 constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
@@ -73,11 +74,20 @@ constexpr int WN = 32;  // warp tile width (4 DMMA column fragments)
 // Padded pitches make every fragment load and every 16-byte staging store
 // conflict-free: a half-warp's 4 k-rows of A (4 n-rows of B) land in 4
 // distinct 32-byte bank groups (pitch = 4 mod 16 doubles).
-constexpr int AP = BM + 4;  // A slab: [BK][AP]   (m contiguous, as in HBM)
+constexpr int AP_MAX = TILE_M + 4;  // A slab: [BK][BM+4] (m contiguous, as in HBM)
 constexpr int BP = BK + 4;  // B slab: [BN][BP]   (k contiguous, as in HBM)
-constexpr int A_STAGE = BK * AP;
-constexpr int B_STAGE = TILE_N * BP;  // sized for the widest CTA
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+// Ring geometry per CTA shape: the smaller the unit, the more (smaller)
+// stages fit, which keeps ~STAGES x slab-time of prefetch ahead of the
+// consumers (5 stages for 128x128, 13 for 64x32).
+template <int BM, int BN>
+struct Ring {
+  static constexpr int A_ST = BK * (BM + 4);  // doubles per A slab
+  static constexpr int B_ST = BN * BP;        // doubles per B slab
+  static constexpr int STAGES_FIT = SMEM_BUDGET / ((A_ST + B_ST) * 8);
+  static constexpr int STAGES = STAGES_FIT < MAX_STAGES ? STAGES_FIT : MAX_STAGES;
+  static constexpr int BYTES = STAGES * (A_ST + B_ST) * 8;
+  static_assert(STAGES >= 3, "ring too shallow");
+};
 constexpr int GROUP_M = MYD_FAST_GROUP_M;
 constexpr int KSTEPS = BK / 4;                  // DMMA k-steps per slab
 constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier is probed
@@ -93,13 +103,17 @@ constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BN>
+template <int VEC, int BM, int BN>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                       int units) {
   using namespace fast;
-  constexpr int SPLIT = TILE_N / BN;
+  constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
+  constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
+  constexpr int AP = BM + 4;                // A pitch: 4 mod 16 doubles (conflict-free)
+  constexpr int STAGES = Ring<BM, BN>::STAGES;
+  constexpr int A_STAGE = Ring<BM, BN>::A_ST, B_STAGE = Ring<BM, BN>::B_ST;
   constexpr int WARPS_N = BN / WN;
   constexpr int WARPS_M = CONSUMER_WARPS / WARPS_N;
   constexpr int WM = BM / WARPS_M;
@@ -110,19 +124,19 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   extern __shared__ __align__(128) double smem[];
   double *As = smem;
   double *Bs = smem + STAGES * A_STAGE;
-  __shared__ __align__(8) uint64_t full_bar[STAGES];
-  __shared__ __align__(8) uint64_t empty_bar[STAGES];
+  __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[MAX_STAGES];
 
   // Work unit u (persistent CTA b takes u = b, b + gridDim.x, ...): full
-  // tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows per band,
-  // column-major inside a band), column strip u % SPLIT of it.
+  // 128x128 tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows
+  // per band, column-major inside a band), sub-block u % SPLIT of it.
   auto unit_origin = [&](int u, int &m0, int &n0) {
-    const int tile = tile0 + u / SPLIT;
+    const int tile = tile0 + u / SPLIT, sub = u % SPLIT;
     const int band = GROUP_M * tiles_n;
     const int first_m = (tile / band) * GROUP_M;
     const int gm = min(tiles_m - first_m, GROUP_M);
-    m0 = (first_m + (tile % band) % gm) * BM;
-    n0 = ((tile % band) / gm) * TILE_N + (u % SPLIT) * BN;
+    m0 = (first_m + (tile % band) % gm) * TILE_M + (sub / SPLIT_N) * BM;
+    n0 = ((tile % band) / gm) * TILE_N + (sub % SPLIT_N) * BN;
   };
 
   const int tid = threadIdx.x;
@@ -339,7 +353,7 @@ namespace {
 
 int sm_count();
 
-template <int VEC, int BN>
+template <int VEC, int BM, int BN>
 cudaError_t launch_one(unsigned units, int M, int N, int K, const double *A, int64_t lda, const double *B,
                        int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, cudaStream_t st) {
   using namespace fast;
@@ -351,14 +365,15 @@ cudaError_t launch_one(unsigned units, int M, int N, int K, const double *A, int
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     cudaError_t e =
-        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Ring<BM, BN>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
   }
   // persistent: at most one CTA per SM, each walking units b, b+grid, ...
   const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
-  dgemm_fast_kernel<VEC, BN>
-      <<<grid, THREADS, SMEM_BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units);
+  dgemm_fast_kernel<VEC, BM, BN>
+      <<<grid, THREADS, Ring<BM, BN>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units);
   count_launch();
   return cudaGetLastError();
 }
@@ -367,10 +382,11 @@ template <int VEC>
 cudaError_t launch_split(int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                          cudaStream_t st) {
-  switch (split) {
-    case 1: return launch_one<VEC, 128>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 2: return launch_one<VEC, 64>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    default: return launch_one<VEC, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+  switch (split) {  // units per 128x128 tile
+    case 1: return launch_one<VEC, 128, 128>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 2: return launch_one<VEC, 128, 64>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 4: return launch_one<VEC, 128, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    default: return launch_one<VEC, 64, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
   }
 }
 
@@ -389,29 +405,32 @@ int sm_count() {
 
 }  // namespace
 
-// Launch plan.  With G SMs (one CTA each) and T full tiles, T = q*G + r:
-// the first q*G tiles run as full 128x128 tiles; the r leftovers are cut into
-// `split` column strips (128x64 or 128x32, still 8 busy warps) when that
-// shortens the last wave: its cost is ceil(r*split/G)/split tile-times.
-// force_split (0 = plan) pins the strip width for tests.
+// Launch plan.  With G SMs (one persistent CTA each) and T full 128x128
+// tiles, T = q*G + r: q*G tiles run as full tiles; the r leftovers are cut
+// into `split` units (128x64, 128x32 or 64x32; all 8 consumer warps busy)
+// when that shortens the last wave, whose cost is ceil(r*split/G)/split
+// tile-times.  Small problems (q = 0) therefore run entirely as small units.
+// force_split (0 = plan) pins the unit shape for tests.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split) {
   using namespace fast;
-  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + TILE_N - 1) / TILE_N;
+  const int tiles_m = (M + TILE_M - 1) / TILE_M, tiles_n = (N + TILE_N - 1) / TILE_N;
   const long long tiles = (long long)tiles_m * tiles_n;
-  if (tiles > 0x7fffffffLL / 4) return cudaErrorInvalidConfiguration;
+  if (tiles > 0x7fffffffLL / 8) return cudaErrorInvalidConfiguration;
   const bool vec2 =
       !force_vec1 && (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
   const long long G = sm_count();
   long long q = tiles / G, r = tiles % G;
   int split = 1;
   if (force_split > 1) {
-    split = force_split >= 4 ? 4 : 2;  // every tile as strips
+    split = force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2);  // every tile as units
     q = 0;
     r = tiles;
   } else if (r > 0) {
     double best = 1.0;
-    for (int s : {2, 4}) {
+    for (int s : {2, 4, 8}) {
+      // 64-high units only pay off when they fill otherwise idle SMs
+      if (s == 8 && q > 0) continue;
       const double cost = (double)((r * s + G - 1) / G) / s;
       if (cost < best - 1e-9) {
         best = cost;
@@ -425,9 +444,10 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     e = vec2 ? launch_split<2>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream)
              : launch_split<1>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream);
   if (e != cudaSuccess || split == 1) return e;
-  const unsigned grid = (unsigned)((tiles - main_tiles) * split);
-  return vec2 ? launch_split<2>(split, grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles, stream)
-              : launch_split<1>(split, grid, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
+  const unsigned units = (unsigned)((tiles - main_tiles) * split);
+  return vec2 ? launch_split<2>(split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
+                                stream)
+              : launch_split<1>(split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
                                 stream);
 }
 

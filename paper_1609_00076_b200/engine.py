@@ -128,7 +128,7 @@ def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, str
     f = _capi.EXACT if exact else 0
     f |= _capi.FORCE_TILED if force_tiled else 0
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
-    f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4}[strips]
+    f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8}[strips]
     return f
 
 
@@ -208,7 +208,8 @@ def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int
                  stream: int = 0, exact: bool = False, force_tiled: bool = False,
                  force_vec1: bool = False, strips: int = 0) -> None:
     """Raw device-pointer call (asynchronous on `stream`).  `strips` (2 or 4)
-    forces every tile through the narrow-strip kernels (tests)."""
+    forces every tile through the narrow-strip kernels, 8 through the 64x32
+    units (tests)."""
     lib = _capi.load()
     _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
                                 _flags(exact, force_tiled, force_vec1, strips) | _capi.DEVICE_PTRS,

@@ -200,21 +200,21 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
     (2304, 2304, 128, 2304, 128, 2304),     # plan picks tail strips (324 tiles)
 ])
 def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
-    """Full tiles, 128x64 strips and 128x32 strips give bitwise the same C
-    (the per-element DMMA sequence does not depend on the CTA shape)."""
+    """Full tiles, 128x64 strips, 128x32 strips and 64x32 units give bitwise
+    the same C (the per-element DMMA sequence does not depend on the CTA shape)."""
     a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
     outs = []
-    for strips in (0, 2, 4):
+    for strips in (0, 2, 4, 8):
         cc = c.clone()
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips)
         outs.append(cc)
-    assert torch_cuda.equal(outs[0], outs[1]) and torch_cuda.equal(outs[0], outs[2])
+    assert all(torch_cuda.equal(outs[0], o) for o in outs[1:])
     ce = c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
     bound = HEADLINE_C * k * EPS * (k + 1)
     mx, i, j = engine.max_abs_diff_device(m, n, outs[0].data_ptr(), ldc, ce.data_ptr(), ldc, bound)
     assert i is None, (i, j, mx)
-    host = outs[2].cpu().numpy()
+    host = outs[3].cpu().numpy()
     if ldc > m:
         assert np.all(host.reshape(n, ldc)[:, m:] == -777.25)
 
