@@ -7,7 +7,7 @@
 //                         A and B panels in the 126 MB L2; the last partial
 //                         wave is re-cut into 128x64 / 128x32 strips so every
 //                         SM gets work (launch_dgemm_fast);
-//   loop 4 (pc)        -> the in-CTA K loop over BK=16 slabs;
+//   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs (16 for full tiles);
 //   pack_a / pack_b    -> producer warps stage each A and B slab into a
 //                         multi-stage shared-memory ring: bulk copies by the
 //                         TMA engine (cp.async.bulk, one per A k-row and per
@@ -46,9 +46,6 @@ __device__ unsigned long long g_fast_prof[8];
 #endif
 
 namespace fast {
-#ifndef MYD_FAST_BK
-#define MYD_FAST_BK 16
-#endif
 #ifndef MYD_FAST_SMEM_KB
 #define MYD_FAST_SMEM_KB 200
 #endif
@@ -57,7 +54,6 @@ namespace fast {
 #endif
 constexpr int TILE_M = 128;              // full CTA tile rows (m); small-problem units are 64 high
 constexpr int TILE_N = 128;              // full CTA tile cols (n); strips are TILE_N / split wide
-constexpr int BK = MYD_FAST_BK;          // K slab per pipeline stage
 constexpr int MAX_STAGES = 16;                        // ring depth cap (mbarrier arrays)
 constexpr int SMEM_BUDGET = MYD_FAST_SMEM_KB * 1024;  // ring bytes per CTA
 constexpr int CONSUMER_WARPS = 8;        // 2 per SM sub-partition
@@ -74,23 +70,28 @@ constexpr int WN = 32;  // warp tile width (4 DMMA column fragments)
 // Padded pitches make every fragment load and every 16-byte staging store
 // conflict-free: a half-warp's 4 k-rows of A (4 n-rows of B) land in 4
 // distinct 32-byte bank groups (pitch = 4 mod 16 doubles).
-constexpr int AP_MAX = TILE_M + 4;  // A slab: [BK][BM+4] (m contiguous, as in HBM)
-constexpr int BP = BK + 4;  // B slab: [BN][BP]   (k contiguous, as in HBM)
-// Ring geometry per CTA shape: the smaller the unit, the more (smaller)
-// stages fit, which keeps ~STAGES x slab-time of prefetch ahead of the
-// consumers (5 stages for 128x128, 13 for 64x32).
+// Ring geometry per CTA shape.  The K slab grows as the unit shrinks so
+// every consumer warp still issues >= 64 DMMAs per slab (the per-slab
+// barrier probe and release cost ~200 cycles): 16 for 128x128 / 128x64,
+// 32 for 128x32, 64 for 64x32.  As many stages as fit the budget.
+// Pitches are 4 mod 16 doubles so fragment loads and 16-byte staging
+// stores are bank-conflict free: A slab [BK][BM+4] (m contiguous, as in
+// HBM), B slab [BN][BK+4] (k contiguous, as in HBM).
 template <int BM, int BN>
 struct Ring {
-  static constexpr int A_ST = BK * (BM + 4);  // doubles per A slab
-  static constexpr int B_ST = BN * BP;        // doubles per B slab
+  static constexpr int WARP_DMMAS = (BM * BN) / (CONSUMER_WARPS * 64);  // DMMAs per warp per k-step
+  static constexpr int BK = WARP_DMMAS >= 16 ? 16 : (WARP_DMMAS >= 8 ? 32 : 64);
+  static constexpr int AP = BM + 4;
+  static constexpr int BP = BK + 4;
+  static constexpr int A_ST = BK * AP;  // doubles per A slab
+  static constexpr int B_ST = BN * BP;  // doubles per B slab
   static constexpr int STAGES_FIT = SMEM_BUDGET / ((A_ST + B_ST) * 8);
   static constexpr int STAGES = STAGES_FIT < MAX_STAGES ? STAGES_FIT : MAX_STAGES;
   static constexpr int BYTES = STAGES * (A_ST + B_ST) * 8;
   static_assert(STAGES >= 3, "ring too shallow");
 };
 constexpr int GROUP_M = MYD_FAST_GROUP_M;
-constexpr int KSTEPS = BK / 4;                  // DMMA k-steps per slab
-constexpr int PROBE_STEP = KSTEPS > 2 ? 1 : 0;  // where the next slab's barrier is probed
+constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is probed
 }  // namespace fast
 
 // VEC: doubles per LDGSTS (2: 16-byte copies and the bulk path, needs even
@@ -111,7 +112,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
   constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
-  constexpr int AP = BM + 4;                // A pitch: 4 mod 16 doubles (conflict-free)
+  constexpr int BK = Ring<BM, BN>::BK;         // K slab per stage
+  constexpr int KSTEPS = BK / 4;               // DMMA k-steps per slab
+  constexpr int AP = Ring<BM, BN>::AP, BP = Ring<BM, BN>::BP;
   constexpr int STAGES = Ring<BM, BN>::STAGES;
   constexpr int A_STAGE = Ring<BM, BN>::A_ST, B_STAGE = Ring<BM, BN>::B_ST;
   constexpr int WARPS_N = BN / WN;
