@@ -72,6 +72,20 @@ MY_DGEMM_API int my_dgemm_ex(int m, int n, int k, const double *A, int lda, cons
                 unsigned flags, void *stream);
 
 /*
+ * Full BLAS dgemm surface: C := alpha * op(A) * op(B) + beta * C with
+ * op(X) = X ('N') or X^T ('T'/'C'); the interface of PAPER.md:542-556, which
+ * the reference leaves out of scope.  Reference-BLAS argument
+ * rules: status -i names the first invalid parameter i (1 transa, 2 transb,
+ * 3 m, 4 n, 5 k, 7 A, 8 lda, 9 B, 10 ldb, 12 C, 13 ldc, 14 flags); m, n or
+ * k = 0 and alpha = 0 are legal (quick return / C := beta C, C not read when
+ * beta = 0).  With alpha = beta = 1 the result is bitwise my_dgemm_ex on
+ * op(A), op(B).  Flags as for my_dgemm_ex (MY_DGEMM_EXACT only with
+ * alpha = beta = 1).
+ */
+MY_DGEMM_API int my_dgemm_blas(char transa, char transb, int m, int n, int k, double alpha, const double *A, int lda,
+                  const double *B, int ldb, double beta, double *C, int ldc, unsigned flags, void *stream);
+
+/*
  * jc-sharded piece of a multi-GPU GEMM: the caller's rank computes
  * C[:, j0:j0+nloc] += A[:, p0:p0+kc] * B[p0:p0+kc, j0:j0+nloc] with device
  * pointers already offset by the caller.  Identical to my_dgemm_ex with

@@ -14,6 +14,7 @@ from .engine import (  # noqa: F401
     alloc_matrix,
     b200_factory,
     check_conformal,
+    dgemm,
     dgemm_device,
     fill_random_device,
     gemm_b200,

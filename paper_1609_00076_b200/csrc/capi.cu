@@ -20,13 +20,14 @@
 namespace myd {
 
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
-                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split);
+                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
+                              const Epilogue &ep);
 cudaError_t launch_dgemm_exact(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                                double *C, int64_t ldc, cudaStream_t stream);
 cudaError_t launch_gemv_n1(int M, int K, const double *A, int64_t lda, const double *b, double *C,
-                           cudaStream_t stream);
+                           cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
-                           int64_t ldc, cudaStream_t stream);
+                           int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
                                cudaStream_t stream);
 cudaError_t launch_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
@@ -34,6 +35,21 @@ cudaError_t launch_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t l
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+// Device-pointer dispatch: picks the kernel for the shape.
+cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                     int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep) {
+  if (flags & MY_DGEMM_EXACT) return launch_dgemm_exact(m, n, k, A, lda, B, ldb, C, ldc, st);
+  if (!(flags & MY_DGEMM_FORCE_TILED)) {
+    if (n == 1) return launch_gemv_n1(m, k, A, lda, B, C, st, ep);
+    if (m == 1) return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st, ep);
+  }
+  const int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
+                    : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
+                    : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
+                                                       : 0;
+  return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, (flags & MY_DGEMM_FORCE_VEC1) != 0, split, ep);
+}
 
 }  // namespace myd
 
@@ -86,19 +102,9 @@ int validate(int m, int n, int k, const void *A, int lda, const void *B, int ldb
   return 0;
 }
 
-// Device-pointer dispatch: picks the kernel for the shape.
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags) {
-  if (flags & MY_DGEMM_EXACT) return launch_dgemm_exact(m, n, k, A, lda, B, ldb, C, ldc, st);
-  if (!(flags & MY_DGEMM_FORCE_TILED)) {
-    if (n == 1) return launch_gemv_n1(m, k, A, lda, B, C, st);
-    if (m == 1) return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st);
-  }
-  const int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
-                    : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
-                    : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
-                                                       : 0;
-  return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, (flags & MY_DGEMM_FORCE_VEC1) != 0, split);
+  return myd::dispatch(m, n, k, A, lda, B, ldb, C, ldc, st, flags, Epilogue{});
 }
 
 // ---- host-pointer path: cached per-device workspace, panel pipeline ----
@@ -235,6 +241,12 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
 }
 
 }  // namespace
+
+namespace myd {
+int capi_fail(int status, const std::string &msg) { return fail(status, msg); }
+int capi_ok() { return ok(); }
+int capi_cuda_fail(cudaError_t e, const char *where) { return cuda_fail(e, where); }
+}  // namespace myd
 
 extern "C" {
 

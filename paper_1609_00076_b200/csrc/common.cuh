@@ -109,6 +109,15 @@ MYD_DEVICE void dmma_884(double &c0, double &c1, double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// Epilogue mode of the GEMM kernels.  blas == 0: the my_dgemm contract,
+// accumulate onto C (the accumulator starts at C, like _mk).  blas == 1:
+// the BLAS dgemm contract, C := alpha * (A B) + beta * C with the product
+// accumulated from zero and C not read when beta == 0.
+struct Epilogue {
+  double alpha = 1.0, beta = 1.0;
+  int blas = 0;
+};
+
 // Kernel launch counter shared by every launcher (my_dgemm_kernel_launches).
 void count_launch(int n = 1);
 

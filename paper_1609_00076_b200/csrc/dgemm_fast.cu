@@ -119,7 +119,7 @@ template <int VEC, int BM, int BN, int BKT>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
-                      int units) {
+                      int units, Epilogue ep) {
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
   constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
@@ -306,9 +306,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         for (int e = 0; e < 2; ++e) {
           const int row = row0 + i * 8, col = col0 + j * 8 + e;
 #ifdef MYD_FAST_CLOAD_CG
-          acc[i][j][e] = (row < M && col < N) ? __ldcg(C + (int64_t)col * ldc + row) : 0.0;
+          acc[i][j][e] = (!ep.blas && row < M && col < N) ? __ldcg(C + (int64_t)col * ldc + row) : 0.0;
 #else
-          acc[i][j][e] = (row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
+          acc[i][j][e] = (!ep.blas && row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
 #endif
         }
 #ifdef MYD_FAST_PROFILE
@@ -378,7 +378,13 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int row = row0 + i * 8, col = col0 + j * 8 + e;
-          if (row < M && col < N) C[(int64_t)col * ldc + row] = acc[i][j][e];
+          if (row < M && col < N) {
+            double *cp = C + (int64_t)col * ldc + row;
+            if (!ep.blas)
+              *cp = acc[i][j][e];
+            else  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
+              *cp = ep.beta == 0.0 ? ep.alpha * acc[i][j][e] : fma(ep.alpha, acc[i][j][e], ep.beta * *cp);
+          }
         }
   }
 }
@@ -388,7 +394,8 @@ namespace {
 int sm_count();
 
 template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>()>
-cudaError_t launch_one(unsigned units, int M, int N, int K, const double *A, int64_t lda, const double *B,
+cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
+                       const double *B,
                        int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, cudaStream_t st) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
@@ -407,25 +414,26 @@ cudaError_t launch_one(unsigned units, int M, int N, int K, const double *A, int
   // persistent: at most one CTA per SM, each walking units b, b+grid, ...
   const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
   dgemm_fast_kernel<VEC, BM, BN, BK>
-      <<<grid, THREADS, Ring<BM, BN, BK>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units);
+      <<<grid, THREADS, Ring<BM, BN, BK>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units,
+                                                          ep);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int VEC>
-cudaError_t launch_split(int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
+cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                          cudaStream_t st) {
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
         if (K >= 1024)  // long K: deeper slabs, fewer ring handshakes
-          return launch_one<VEC, 128, 128, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
       }
-      return launch_one<VEC, 128, 128, 16>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 2: return launch_one<VEC, 128, 64>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 4: return launch_one<VEC, 128, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    default: return launch_one<VEC, 64, 32>(units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
   }
 }
 
@@ -451,7 +459,8 @@ int sm_count() {
 // tile-times.  Small problems (q = 0) therefore run entirely as small units.
 // force_split (0 = plan) pins the unit shape for tests.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
-                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split) {
+                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
+                              const Epilogue &ep) {
   using namespace fast;
   const int tiles_m = (M + TILE_M - 1) / TILE_M, tiles_n = (N + TILE_N - 1) / TILE_N;
   const long long tiles = (long long)tiles_m * tiles_n;
@@ -480,13 +489,13 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   const long long main_tiles = split == 1 ? tiles : q * G;
   cudaError_t e = cudaSuccess;
   if (main_tiles > 0)
-    e = vec2 ? launch_split<2>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream)
-             : launch_split<1>(1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream);
+    e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream)
+             : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream);
   if (e != cudaSuccess || split == 1) return e;
   const unsigned units = (unsigned)((tiles - main_tiles) * split);
-  return vec2 ? launch_split<2>(split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
+  return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
                                 stream)
-              : launch_split<1>(split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
+              : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
                                 stream);
 }
 

@@ -34,7 +34,7 @@ namespace myd {
 template <int WARPS, int UNROLL>
 __global__ void __launch_bounds__(32 * WARPS)
     gemv_n1_kernel(int M, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ b,
-                   double *__restrict__ C) {
+                   double *__restrict__ C, Epilogue ep) {
   __shared__ double part[WARPS][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = blockIdx.x * 32 + lane;
@@ -59,10 +59,17 @@ __global__ void __launch_bounds__(32 * WARPS)
   part[warp][lane] = acc;
   __syncthreads();
   if (warp == 0 && row < M) {
-    double s = C[row];
+    if (!ep.blas) {
+      double s = C[row];
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) s += part[w][lane];
-    C[row] = s;
+      for (int w = 0; w < WARPS; ++w) s += part[w][lane];
+      C[row] = s;
+    } else {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) s += part[w][lane];
+      C[row] = ep.beta == 0.0 ? ep.alpha * s : fma(ep.alpha, s, ep.beta * C[row]);
+    }
   }
 }
 
@@ -78,7 +85,7 @@ constexpr int M1_TEAMS = 8;  // teams per CTA (8 x TEAM warps)
 template <int TEAM, int UNROLL, bool STAGED>
 __global__ void __launch_bounds__(32 * TEAM * M1_TEAMS, 1)
     gemv_m1_kernel(int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
-                   double *__restrict__ C, int64_t ldc) {
+                   double *__restrict__ C, int64_t ldc, Epilogue ep) {
   extern __shared__ double arow[];  // K doubles when STAGED
   __shared__ double part[2][M1_TEAMS][TEAM];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -112,9 +119,10 @@ __global__ void __launch_bounds__(32 * TEAM * M1_TEAMS, 1)
     // team barrier (ids 1..M1_TEAMS; 0 is __syncthreads)
     asm volatile("bar.sync %0, %1;\n" ::"r"(1 + team), "r"(32 * TEAM) : "memory");
     if (t == 0 && lane == 0) {
-      double s = C[j * ldc];
+      double s = ep.blas ? 0.0 : C[j * ldc];
 #pragma unroll
       for (int w = 0; w < TEAM; ++w) s += part[buf][team][w];
+      if (ep.blas) s = ep.beta == 0.0 ? ep.alpha * s : fma(ep.alpha, s, ep.beta * C[j * ldc]);
       C[j * ldc] = s;
     }
   }
@@ -130,14 +138,14 @@ int sm_count_skinny() {
 }  // namespace
 
 cudaError_t launch_gemv_n1(int M, int K, const double *A, int64_t lda, const double *b, double *C,
-                           cudaStream_t stream) {
-  gemv_n1_kernel<MYD_N1_WARPS, MYD_N1_UNROLL><<<(M + 31) / 32, 32 * MYD_N1_WARPS, 0, stream>>>(M, K, A, lda, b, C);
+                           cudaStream_t stream, const Epilogue &ep) {
+  gemv_n1_kernel<MYD_N1_WARPS, MYD_N1_UNROLL><<<(M + 31) / 32, 32 * MYD_N1_WARPS, 0, stream>>>(M, K, A, lda, b, C, ep);
   count_launch();
   return cudaGetLastError();
 }
 
 cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
-                           int64_t ldc, cudaStream_t stream) {
+                           int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
   constexpr int TEAM = MYD_M1_TEAM;
   const int threads = 32 * TEAM * M1_TEAMS;
   const int64_t want = (N + M1_TEAMS - 1) / M1_TEAMS;
@@ -155,9 +163,9 @@ cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const dou
       if (e != cudaSuccess) return e;
       attr_done.fetch_or(bit, std::memory_order_release);
     }
-    gemv_m1_kernel<TEAM, MYD_M1_UNROLL, true><<<grid, threads, smem, stream>>>(N, K, A, lda, B, ldb, C, ldc);
+    gemv_m1_kernel<TEAM, MYD_M1_UNROLL, true><<<grid, threads, smem, stream>>>(N, K, A, lda, B, ldb, C, ldc, ep);
   } else {
-    gemv_m1_kernel<TEAM, MYD_M1_UNROLL, false><<<grid, threads, 0, stream>>>(N, K, A, lda, B, ldb, C, ldc);
+    gemv_m1_kernel<TEAM, MYD_M1_UNROLL, false><<<grid, threads, 0, stream>>>(N, K, A, lda, B, ldb, C, ldc, ep);
   }
   count_launch();
   return cudaGetLastError();

@@ -46,6 +46,7 @@ __all__ = [
     "operand_seed",
     "max_abs_diff_device",
     "kernel_launches",
+    "dgemm",
 ]
 
 
@@ -245,3 +246,28 @@ def max_abs_diff_device(m: int, n: int, x_ptr: int, ldx: int, y_ptr: int, ldy: i
 
 def kernel_launches() -> int:
     return int(_capi.load().my_dgemm_kernel_launches())
+
+
+def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A, lda: int, B, ldb: int,
+          beta: float, C, ldc: int, exact: bool = False, stream: int | None = None):
+    """BLAS dgemm: C := alpha op(A) op(B) + beta C.
+
+    Host numpy buffers (synchronous) or torch CUDA tensors (asynchronous on
+    `stream`, default torch's current stream).  Argument errors raise
+    ValueError naming the BLAS parameter.
+    """
+    lib = _capi.load()
+    flags = _flags(exact)
+    dev = _is_device(C)
+    if dev:
+        if stream is None:
+            import torch
+
+            stream = torch.cuda.current_stream(C.device).cuda_stream
+        flags |= _capi.DEVICE_PTRS
+    ptr = lambda x: None if x is None else _ptr(x)  # noqa: E731
+    st = lib.my_dgemm_blas(transa.encode()[:1], transb.encode()[:1], m, n, k, float(alpha), ptr(A), lda,
+                           ptr(B), ldb, float(beta), ptr(C), ldc, flags,
+                           ctypes.c_void_p(stream) if dev else None)
+    _capi.check(st)
+    return C

@@ -123,3 +123,40 @@ def test_missing_library_fails_loudly(tmp_path, monkeypatch):
     monkeypatch.setattr(_capi, "_lib", None)
     with pytest.raises(_capi.NativeLibraryError):
         _capi.load(str(tmp_path / "absent.so"))
+
+
+BLAS_BAD = [
+    # (transa, transb, m, n, k, lda, ldb, ldc, status)
+    ("X", "N", 4, 4, 4, 4, 4, 4, -1),
+    ("N", "Q", 4, 4, 4, 4, 4, 4, -2),
+    ("N", "N", -1, 4, 4, 4, 4, 4, -3),
+    ("N", "N", 4, -1, 4, 4, 4, 4, -4),
+    ("N", "N", 4, 4, -1, 4, 4, 4, -5),
+    ("N", "N", 4, 4, 4, 3, 4, 4, -8),
+    ("T", "N", 4, 4, 5, 4, 5, 4, -8),    # A^T: A is k x m, lda >= k
+    ("N", "N", 4, 4, 4, 4, 3, 4, -10),
+    ("N", "T", 4, 5, 4, 4, 4, 4, -10),   # B^T: B is n x k, ldb >= n
+    ("N", "N", 4, 4, 4, 4, 4, 3, -13),
+]
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k,lda,ldb,ldc,status", BLAS_BAD)
+def test_blas_argument_checks_reference_order(lib, ta, tb, m, n, k, lda, ldb, ldc, status):
+    c = np.full(64, 3.5)
+    a = np.ones(64)
+    got = lib.my_dgemm_blas(ta.encode(), tb.encode(), m, n, k, 1.0, a.ctypes.data, lda, a.ctypes.data, ldb, 1.0,
+                            c.ctypes.data, ldc, 0, None)
+    assert got == status
+    assert np.all(c == 3.5)
+
+
+def test_blas_quick_returns_touch_nothing(lib):
+    c = np.full(16, 3.5)
+    # m == 0, n == 0, or (alpha == 0 or k == 0) with beta == 1: no memory touched, no device needed
+    assert lib.my_dgemm_blas(b"N", b"N", 0, 4, 4, 1.0, None, 1, None, 4, 1.0, None, 1, 0, None) == 0
+    assert lib.my_dgemm_blas(b"N", b"N", 4, 0, 4, 1.0, None, 4, None, 4, 1.0, None, 4, 0, None) == 0
+    assert lib.my_dgemm_blas(b"N", b"N", 4, 4, 4, 0.0, None, 4, None, 4, 1.0, c.ctypes.data, 4, 0, None) == 0
+    assert lib.my_dgemm_blas(b"N", b"N", 4, 4, 0, 2.0, None, 4, None, 1, 1.0, c.ctypes.data, 4, 0, None) == 0
+    assert np.all(c == 3.5)
+    with pytest.raises(ValueError, match="EXACT"):
+        engine.dgemm("N", "N", 2, 2, 2, 2.0, np.ones(4), 2, np.ones(4), 2, 1.0, np.ones(4), 2, exact=True)

@@ -339,3 +339,65 @@ def test_host_path_pipeline_bitwise_equals_device_path(torch_cuda, m, n, k, lda,
     dev = dc.cpu().numpy()
     assert np.array_equal(oracle.valid_region(got, m, n, ldc), oracle.valid_region(dev, m, n, ldc))
     assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
+
+
+# ------------------------------------------------------------ BLAS surface
+
+
+def blas_reference(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc):
+    """alpha op(A) op(B) + beta C via the oracle on explicitly transposed
+    operands (products p-ascending), plus the headline bound."""
+    A = oracle.valid_region(a, k if ta == "T" else m, m if ta == "T" else k, lda).T
+    B = oracle.valid_region(b, n if tb == "T" else k, k if tb == "T" else n, ldb).T
+    opA = np.ascontiguousarray((A.T if ta == "T" else A).T).ravel()   # column-major m x k
+    opB = np.ascontiguousarray((B.T if tb == "T" else B).T).ravel()   # column-major k x n
+    P = oracle.naive(m, n, k, opA, m, opB, k, np.zeros(m * n), m)
+    Cv = oracle.valid_region(c, m, n, ldc)
+    want = alpha * P.reshape(n, m) + (beta * Cv if beta != 0 else 0.0)
+    mag = abs(alpha) * (np.abs(opA.reshape(k, m).T) @ np.abs(opB.reshape(n, k).T))
+    if beta != 0:
+        mag = mag + abs(beta) * np.abs(Cv.T)
+    return want, (HEADLINE_C * (k + 2) * EPS * float(mag.max()) if mag.size else 0.0)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+@pytest.mark.parametrize("alpha,beta", [(1.0, 1.0), (-0.5, 2.0), (1.5, 0.0), (0.0, -3.0)])
+@pytest.mark.parametrize("m,n,k", [(37, 53, 71), (300, 1, 257), (1, 300, 257), (130, 260, 190)])
+def test_blas_dgemm_host(torch_cuda, ta, tb, alpha, beta, m, n, k):
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    nra, nca = (k, m) if ta == "T" else (m, k)
+    nrb, ncb = (n, k) if tb == "T" else (k, n)
+    lda, ldb, ldc = nra + 3, nrb + 1, m + 2
+    a = rng.uniform(-1, 1, lda * nca)
+    b = rng.uniform(-1, 1, ldb * ncb)
+    c = rng.uniform(-1, 1, ldc * n)
+    c.reshape(n, ldc)[:, m:] = -777.25
+    if beta == 0.0:
+        c.reshape(n, ldc)[:, :m] = np.nan   # must not be read
+    want, bound = blas_reference(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc)
+    got = engine.dgemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c.copy(), ldc)
+    gv = oracle.valid_region(got, m, n, ldc)
+    assert np.all(np.isfinite(gv))
+    assert np.abs(gv - want).max() <= bound + 1e-300
+    assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
+
+
+def test_blas_alpha_beta_one_is_bitwise_my_dgemm_on_transposed_operands(torch_cuda):
+    """op(A) via the transpose pre-pass is the NN kernel on A^T: bitwise."""
+    m, n, k = 700, 500, 300
+    a, b, c, _ = dev_operands(torch_cuda, k, n, m)          # A stored k x m (to be transposed)
+    bt = dev_matrix(torch_cuda, n, k, n, 99)                # B stored n x k
+    at = a[: k * m].view(m, k).t().contiguous().view(-1)    # explicit A^T, column-major m x k
+    btt = bt[: n * k].view(k, n).t().contiguous().view(-1)  # explicit B^T, k x n
+    c0 = torch_cuda.rand(m * n, dtype=torch_cuda.float64, device="cuda")
+    c1, c2 = c0.clone(), c0.clone()
+    engine.dgemm("T", "T", m, n, k, 1.0, a, k, bt, n, 1.0, c1, m)
+    run_dev(torch_cuda, m, n, k, at, m, btt, k, c2, m)
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(c1, c2)
+    c3 = c0.clone()
+    engine.dgemm("T", "T", m, n, k, 1.0, a, k, bt, n, 1.0, c3, m, exact=True)
+    c4 = c0.clone()
+    run_dev(torch_cuda, m, n, k, at, m, btt, k, c4, m, exact=True)
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(c3, c4)
