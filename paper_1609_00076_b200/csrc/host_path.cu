@@ -1,0 +1,393 @@
+// host_path.cu -- my_dgemm on HOST pointers: the drop-in CPU signature
+// driving the device kernels, with the transfers pipelined
+// against the GEMM.
+//
+// Measured on the B200 box (tools/pcie_probe.py): PCIe 5 moves 55.5 GB/s
+// H2D and 56.8 GB/s D2H from pinned memory but only ~34 GB/s in total when
+// both directions run at once, and 26.7 / 17.5 GB/s from pageable memory.
+// Schedule (modelled by tools/e2e_schedule_sim.py):
+//   * uploads first, downloads deferred until every upload is queued;
+//   * the first column group (half of C) is computed in k-chunks while A is
+//     still uploading (chunks are multiples of 16: bitwise the unchunked
+//     result), the remaining panels run whole as their B and C land;
+//   * each panel's C goes down as soon as it is final.
+// Pageable callers (numpy arrays, the reference's own Matrix objects) go
+// through a pinned staging ring filled and drained by a small pool of host
+// threads, so the DMA engines always see pinned memory.  Copies are pitched
+// (width rows*8): padding rows are never read or written and nothing past
+// (n-1)*ld+m is touched (matrix.py:5-6,42-45,58-61).
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/my_dgemm.h"
+#include "common.cuh"
+
+namespace myd {
+
+cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                     int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep);
+int capi_fail(int status, const std::string &msg);
+int capi_ok();
+int capi_cuda_fail(cudaError_t e, const char *where);
+
+namespace {
+
+// ---- a small fork-free host thread pool for pitched copies ----
+class CopyPool {
+ public:
+  static CopyPool &get() {
+    static CopyPool pool;
+    return pool;
+  }
+  // Run fn(i) for i in [0, n) on the pool and the calling thread; blocks.
+  void parallel_for(int n, const std::function<void(int)> &fn) {
+    if (n <= 1 || workers_.empty()) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &fn;
+    total_ = n;
+    next_.store(0);
+    done_ = 0;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    work();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return done_ == total_; });
+    job_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    int want = 8;
+    if (const char *s = getenv("MY_DGEMM_HOST_THREADS")) want = std::max(1, atoi(s));
+    const int hw = (int)std::thread::hardware_concurrency();
+    if (hw > 0) want = std::min(want, hw);
+    for (int t = 1; t < want; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
+      if (stop_) return;
+      seen = gen_;
+      lk.unlock();
+      work();
+    }
+  }
+  void work() {
+    const std::function<void(int)> *fn = job_;
+    int did = 0;
+    for (int i = next_.fetch_add(1); i < total_; i = next_.fetch_add(1)) {
+      (*fn)(i);
+      ++did;
+    }
+    if (did) {
+      std::lock_guard<std::mutex> lk(mu_);
+      done_ += did;
+      if (done_ == total_) done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)> *job_ = nullptr;
+  std::atomic<int> next_{0};
+  int total_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// pitched host copy of `cols` columns of `rows` doubles, split over the pool
+void host_copy_2d(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols) {
+  const int64_t bytes = rows * 8;
+  const int64_t per = std::max<int64_t>(1, (4 << 20) / std::max<int64_t>(bytes, 1));  // ~4 MB per task
+  const int tasks = (int)((cols + per - 1) / per);
+  CopyPool::get().parallel_for(tasks, [&](int t) {
+    const int64_t c0 = t * per, c1 = std::min<int64_t>(cols, c0 + per);
+    for (int64_t c = c0; c < c1; ++c) memcpy(dst + c * dpitch, src + c * spitch, (size_t)bytes);
+  });
+}
+
+struct Workspace {
+  int device = -1;
+  double *dA = nullptr, *dB = nullptr, *dC = nullptr;
+  size_t capA = 0, capB = 0, capC = 0;
+  cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done, ev_out;
+  // pinned staging ring for pageable callers
+  static constexpr int NSTAGE = 6;
+  static constexpr size_t STAGE_BYTES = 32u << 20;
+  double *stage[NSTAGE] = {};
+  cudaEvent_t ev_stage[NSTAGE] = {};
+};
+
+std::mutex g_ws_mutex;
+Workspace g_ws[64];
+
+cudaError_t grow(double **p, size_t *cap, size_t need) {
+  if (*cap >= need) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc((void **)p, need);
+  if (e == cudaSuccess) *cap = need;
+  return e;
+}
+
+cudaError_t ensure_streams(Workspace &w, size_t n_events) {
+  cudaError_t e;
+  if (!w.s_h2d) {
+    if ((e = cudaStreamCreateWithFlags(&w.s_h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&w.s_comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&w.s_d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  }
+  while (w.ev_in.size() < n_events) {
+    cudaEvent_t a, b, c;
+    if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&c, cudaEventDisableTiming)) != cudaSuccess) return e;
+    w.ev_in.push_back(a);
+    w.ev_done.push_back(b);
+    w.ev_out.push_back(c);
+  }
+  return cudaSuccess;
+}
+
+cudaError_t ensure_stage(Workspace &w) {
+  cudaError_t e;
+  for (int i = 0; i < Workspace::NSTAGE; ++i) {
+    if (w.stage[i]) continue;
+    if ((e = cudaMallocHost((void **)&w.stage[i], Workspace::STAGE_BYTES)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&w.ev_stage[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+bool is_pinned(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Moves pitched column blocks between host and device on the workspace
+// streams: straight DMA for pinned host memory, through the staging ring for
+// pageable memory (host threads fill/drain the ring; the issuing thread
+// blocks only on the copy work it must do itself).
+class Mover {
+ public:
+  Mover(Workspace &w, bool staged) : w_(w), staged_(staged) {}
+
+  cudaError_t up(double *d, int64_t dpitch, const double *h, int64_t hpitch, int64_t rows, int64_t cols) {
+    if (!staged_ || rows * 8 > (int64_t)Workspace::STAGE_BYTES)  // a column larger than a stage: direct
+      return cudaMemcpy2DAsync(d, dpitch * 8, h, (size_t)hpitch * 8, (size_t)rows * 8, cols,
+                               cudaMemcpyHostToDevice, w_.s_h2d);
+    const int64_t per = std::max<int64_t>(1, (int64_t)(Workspace::STAGE_BYTES / 8) / rows);
+    for (int64_t c0 = 0; c0 < cols; c0 += per) {
+      const int64_t nc = std::min(per, cols - c0);
+      const int s = next();
+      cudaError_t e = cudaEventSynchronize(w_.ev_stage[s]);  // buffer free (its last DMA done)
+      if (e != cudaSuccess) return e;
+      host_copy_2d(w_.stage[s], rows, h + c0 * hpitch, hpitch, rows, nc);
+      e = cudaMemcpy2DAsync(d + c0 * dpitch, dpitch * 8, w_.stage[s], (size_t)rows * 8, (size_t)rows * 8, nc,
+                            cudaMemcpyHostToDevice, w_.s_h2d);
+      if (e != cudaSuccess) return e;
+      if ((e = cudaEventRecord(w_.ev_stage[s], w_.s_h2d)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+
+  // Queue a download; staged pieces are copied out to the user buffer as
+  // their DMA completes (at the latest in finish()).
+  cudaError_t down(double *h, int64_t hpitch, const double *d, int64_t dpitch, int64_t rows, int64_t cols) {
+    if (!staged_ || rows * 8 > (int64_t)Workspace::STAGE_BYTES)
+      return cudaMemcpy2DAsync(h, (size_t)hpitch * 8, d, dpitch * 8, (size_t)rows * 8, cols,
+                               cudaMemcpyDeviceToHost, w_.s_d2h);
+    const int64_t per = std::max<int64_t>(1, (int64_t)(Workspace::STAGE_BYTES / 8) / rows);
+    for (int64_t c0 = 0; c0 < cols; c0 += per) {
+      const int64_t nc = std::min(per, cols - c0);
+      const int s = next();
+      cudaError_t e = drain_until_free(s);
+      if (e != cudaSuccess) return e;
+      e = cudaMemcpy2DAsync(w_.stage[s], (size_t)rows * 8, d + c0 * dpitch, dpitch * 8, (size_t)rows * 8, nc,
+                            cudaMemcpyDeviceToHost, w_.s_d2h);
+      if (e != cudaSuccess) return e;
+      if ((e = cudaEventRecord(w_.ev_stage[s], w_.s_d2h)) != cudaSuccess) return e;
+      pending_.push_back({s, h + c0 * hpitch, hpitch, rows, nc});
+    }
+    return cudaSuccess;
+  }
+
+  cudaError_t finish() {
+    while (!pending_.empty()) {
+      cudaError_t e = pop();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+
+ private:
+  struct Out {
+    int s;
+    double *h;
+    int64_t hpitch, rows, cols;
+  };
+  int next() {
+    const int s = slot_;
+    slot_ = (slot_ + 1) % Workspace::NSTAGE;
+    return s;
+  }
+  cudaError_t pop() {
+    Out o = pending_.front();
+    pending_.pop_front();
+    cudaError_t e = cudaEventSynchronize(w_.ev_stage[o.s]);
+    if (e != cudaSuccess) return e;
+    host_copy_2d(o.h, o.hpitch, w_.stage[o.s], o.rows, o.rows, o.cols);
+    return cudaSuccess;
+  }
+  // Before reusing stage s for a download, copy out (in queue order) every
+  // pending piece up to the one that occupies s.
+  cudaError_t drain_until_free(int s) {
+    auto uses = [&] {
+      for (const Out &o : pending_)
+        if (o.s == s) return true;
+      return false;
+    };
+    while (uses()) {
+      cudaError_t e = pop();
+      if (e != cudaSuccess) return e;
+    }
+    return cudaEventSynchronize(w_.ev_stage[s]);
+  }
+  Workspace &w_;
+  bool staged_;
+  int slot_ = 0;
+  std::deque<Out> pending_;
+};
+
+}  // namespace
+
+int host_path(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc,
+              unsigned flags) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return capi_cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return capi_fail(-11, "device index out of range");
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  Workspace &w = g_ws[dev];
+  w.device = dev;
+  // Device copies use even leading dimensions so every column starts 16-byte
+  // aligned and the bulk-copy staging path applies whatever the host ld was.
+  const int64_t dlda = (m + 1) & ~1LL, dldb = (k + 1) & ~1LL, dldc = (m + 1) & ~1LL;
+  const double flops = 2.0 * m * (double)n * k;
+  const bool pipelined = flops > 4e9 && n >= 1024 && m > 1 && n > 1;
+  int64_t nc0 = n, panel = n;
+  if (pipelined) {
+    nc0 = std::max<int64_t>(128, (n / 2) / 128 * 128);
+    panel = std::max<int64_t>(512, ((n / 8 + 127) / 128) * 128);
+  }
+  const size_t panels = 1 + (size_t)((n - nc0 + panel - 1) / panel);  // group 0 + whole panels
+  auto panel_j0 = [&](size_t p) -> int64_t { return p == 0 ? 0 : nc0 + (int64_t)(p - 1) * panel; };
+  auto panel_nc = [&](size_t p) -> int64_t { return p == 0 ? nc0 : std::min<int64_t>(panel, n - panel_j0(p)); };
+  int64_t kchunk = k;
+  if (pipelined && k >= 256) kchunk = (((k + 7) / 8) + 15) / 16 * 16;
+  const size_t kchunks = (size_t)((k + kchunk - 1) / kchunk);
+  if ((e = ensure_streams(w, std::max(panels, kchunks) + 1)) != cudaSuccess)
+    return capi_cuda_fail(e, "stream setup");
+  if ((e = grow(&w.dA, &w.capA, (size_t)dlda * k * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(A)");
+  if ((e = grow(&w.dB, &w.capB, (size_t)dldb * n * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(B)");
+  if ((e = grow(&w.dC, &w.capC, (size_t)dldc * n * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(C)");
+  const bool staged = !(is_pinned(A) && is_pinned(B) && is_pinned(C));
+  if (staged && (e = ensure_stage(w)) != cudaSuccess) return capi_cuda_fail(e, "pinned staging");
+  Mover mv(w, staged);
+  const Epilogue ep{};
+
+  // Program order = issue order: every GEMM is queued right after the
+  // uploads it needs, so the device never waits for the host to finish
+  // staging unrelated data.
+  if ((e = mv.up(w.dC, dldc, C, ldc, m, nc0)) != cudaSuccess) return capi_cuda_fail(e, "H2D C");
+  for (size_t c = 0; c < kchunks; ++c) {  // group 0: k-chunks as A arrives
+    const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
+    if ((e = mv.up(w.dA + p0 * dlda, dlda, A + p0 * lda, lda, m, kl)) != cudaSuccess)
+      return capi_cuda_fail(e, "H2D A");
+    if ((e = mv.up(w.dB + p0, dldb, B + p0, ldb, kl, nc0)) != cudaSuccess) return capi_cuda_fail(e, "H2D B");
+    cudaEventRecord(w.ev_in[c], w.s_h2d);
+    cudaStreamWaitEvent(w.s_comp, w.ev_in[c], 0);
+    e = dispatch(m, (int)nc0, (int)kl, w.dA + p0 * dlda, dlda, w.dB + p0, dldb, w.dC, dldc, w.s_comp, flags, ep);
+    if (e != cudaSuccess) return capi_cuda_fail(e, "kernel launch");
+  }
+  cudaEventRecord(w.ev_out[0], w.s_comp);
+  for (size_t p = 1; p < panels; ++p) {  // whole panels as their B and C land
+    const int64_t j0 = panel_j0(p), nc = panel_nc(p);
+    if ((e = mv.up(w.dB + j0 * dldb, dldb, B + j0 * ldb, ldb, k, nc)) != cudaSuccess)
+      return capi_cuda_fail(e, "H2D B");
+    if ((e = mv.up(w.dC + j0 * dldc, dldc, C + j0 * ldc, ldc, m, nc)) != cudaSuccess)
+      return capi_cuda_fail(e, "H2D C");
+    cudaEventRecord(w.ev_done[p], w.s_h2d);
+    cudaStreamWaitEvent(w.s_comp, w.ev_done[p], 0);
+    e = dispatch(m, (int)nc, k, w.dA, dlda, w.dB + j0 * dldb, dldb, w.dC + j0 * dldc, dldc, w.s_comp, flags, ep);
+    if (e != cudaSuccess) return capi_cuda_fail(e, "kernel launch");
+    cudaEventRecord(w.ev_out[p], w.s_comp);
+  }
+  cudaEvent_t all_in = w.ev_in[kchunks];  // every upload done: downloads may start
+  cudaEventRecord(all_in, w.s_h2d);
+  cudaStreamWaitEvent(w.s_d2h, all_in, 0);
+  for (size_t p = 0; p < panels; ++p) {
+    const int64_t j0 = panel_j0(p), nc = panel_nc(p);
+    cudaStreamWaitEvent(w.s_d2h, w.ev_out[p], 0);
+    if ((e = mv.down(C + j0 * ldc, ldc, w.dC + j0 * dldc, dldc, m, nc)) != cudaSuccess)
+      return capi_cuda_fail(e, "D2H C");
+  }
+  if ((e = mv.finish()) != cudaSuccess) return capi_cuda_fail(e, "D2H C");
+  if ((e = cudaStreamSynchronize(w.s_d2h)) != cudaSuccess) return capi_cuda_fail(e, "synchronize");
+  if ((e = cudaStreamSynchronize(w.s_comp)) != cudaSuccess) return capi_cuda_fail(e, "synchronize");
+  return capi_ok();
+}
+
+void release_host_workspace() {
+  std::lock_guard<std::mutex> lock(g_ws_mutex);
+  for (auto &w : g_ws) {
+    if (w.device < 0) continue;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(w.device);
+    if (w.dA) cudaFree(w.dA);
+    if (w.dB) cudaFree(w.dB);
+    if (w.dC) cudaFree(w.dC);
+    w.dA = w.dB = w.dC = nullptr;
+    w.capA = w.capB = w.capC = 0;
+    for (int i = 0; i < Workspace::NSTAGE; ++i) {
+      if (w.stage[i]) {
+        if (w.ev_stage[i]) cudaEventSynchronize(w.ev_stage[i]);
+        cudaFreeHost(w.stage[i]);
+      }
+      w.stage[i] = nullptr;
+    }
+    cudaSetDevice(prev);
+  }
+}
+
+}  // namespace myd

@@ -401,3 +401,25 @@ def test_blas_alpha_beta_one_is_bitwise_my_dgemm_on_transposed_operands(torch_cu
     run_dev(torch_cuda, m, n, k, at, m, btt, k, c4, m, exact=True)
     torch_cuda.cuda.synchronize()
     assert torch_cuda.equal(c3, c4)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_host_path_pageable_and_pinned_agree(torch_cuda, pinned):
+    """Pageable callers go through the pinned staging ring; pinned ones DMA
+    directly: both give bitwise the device-path result (odd lds, pipelined)."""
+    m, n, k = 1500, 3000, 1000
+    lda, ldb, ldc = 1507, 1003, 1501
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, lda, ldb, ldc, canary=-777.25)
+    if pinned:
+        ta, tb, tc = (torch_cuda.from_numpy(x).pin_memory() for x in (a, b, c))
+        lib = _capi.load()
+        _capi.check(lib.my_dgemm_ex(m, n, k, ta.data_ptr(), lda, tb.data_ptr(), ldb, tc.data_ptr(), ldc, 0,
+                                    None))
+        got = tc.numpy()
+    else:
+        got = engine.my_dgemm(m, n, k, a, lda, b, ldb, c.copy(), ldc)
+    dc = torch_cuda.from_numpy(c).cuda()
+    run_dev(torch_cuda, m, n, k, torch_cuda.from_numpy(a).cuda(), lda, torch_cuda.from_numpy(b).cuda(), ldb,
+            dc, ldc)
+    assert np.array_equal(oracle.valid_region(got, m, n, ldc), oracle.valid_region(dc.cpu().numpy(), m, n, ldc))
+    assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
