@@ -47,11 +47,8 @@ __device__ unsigned long long g_fast_prof[8];
 #endif
 
 namespace fast {
-#ifndef MYD_FAST_C_PREFETCH
-#define MYD_FAST_C_PREFETCH 1
-#endif
 #ifndef MYD_FAST_SMEM_KB
-#define MYD_FAST_SMEM_KB 216
+#define MYD_FAST_SMEM_KB 224
 #endif
 #ifndef MYD_FAST_GROUP_M
 #define MYD_FAST_GROUP_M 8
@@ -96,10 +93,20 @@ struct Ring {
   static constexpr int BP = BK + 4;
   static constexpr int A_ST = BK * AP;  // doubles per A slab
   static constexpr int B_ST = BN * BP;  // doubles per B slab
+  static constexpr int SLOT = A_ST + B_ST;  // one ring slot: A slab then B slab
+  // A unit's C block is staged through ring slots before its first slab:
+  // CPS columns per slot at pitch CP = BM + 2 (column-pair stride = 32 B mod
+  // 128, so the consumers' C fragment loads are conflict-free), CS slots.
+  static constexpr int CP = BM + 2;
+  static constexpr int CPS = (64 <= BN && 64 * CP <= SLOT) ? 64
+                             : (32 <= BN && 32 * CP <= SLOT) ? 32
+                             : (16 * CP <= SLOT) ? 16 : 8;
+  static constexpr int CS = BN / CPS;
   static constexpr int STAGES_FIT = SMEM_BUDGET / ((A_ST + B_ST) * 8);
   static constexpr int STAGES = STAGES_FIT < MAX_STAGES ? STAGES_FIT : MAX_STAGES;
-  static constexpr int BYTES = STAGES * (A_ST + B_ST) * 8;
+  static constexpr int BYTES = STAGES * SLOT * 8;
   static_assert(STAGES >= 3, "ring too shallow");
+  static_assert(CS < STAGES && BN % CPS == 0 && CPS * CP <= SLOT, "C staging must leave a slab slot");
 };
 constexpr int GROUP_M = MYD_FAST_GROUP_M;
 constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is probed
@@ -128,7 +135,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   constexpr int KSTEPS = BK / 4;     // DMMA k-steps per slab
   constexpr int AP = R::AP, BP = R::BP;
   constexpr int STAGES = R::STAGES;
-  constexpr int A_STAGE = R::A_ST, B_STAGE = R::B_ST;
+  constexpr int SLOT = R::SLOT, A_STAGE = R::A_ST;
+  constexpr int CP = R::CP, CPS = R::CPS, CS = R::CS;
   constexpr int WARPS_N = BN / WN;
   constexpr int WARPS_M = CONSUMER_WARPS / WARPS_N;
   constexpr int WM = BM / WARPS_M;
@@ -136,9 +144,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   constexpr int RW = BN / PRODUCER_WARPS;  // B rows staged by each producer warp
   static_assert(WARPS_M * WARPS_N == CONSUMER_WARPS && FM >= 1 && RW >= 8, "tile shape");
 
-  extern __shared__ __align__(128) double smem[];
-  double *As = smem;
-  double *Bs = smem + STAGES * A_STAGE;
+  extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
   __shared__ __align__(8) uint64_t empty_bar[MAX_STAGES];
 
@@ -172,23 +178,39 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     // ================= producers: pack_a / pack_b equivalent =================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
-    uint32_t g = 0;  // slabs staged by this CTA so far (ring position)
+    const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+    uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int m0, n0;
       unit_origin(u, m0, n0);
-      // Warm L2 with the C tile of this CTA's next unit: its consumers load
-      // it at the start of that unit, right when the ring is already full.
-      if (MYD_FAST_C_PREFETCH && u + (int)gridDim.x < units) {
-        int pm0, pn0;
-        unit_origin(u + gridDim.x, pm0, pn0);
-        const int rows = min(BM, M - pm0);
-        if (pw * RW + (lane % RW) < BN && lane < RW) {
-          const int col = pn0 + pw * RW + lane;
-          if (col < N && rows > 0) {
-            const double *c0 = C + (int64_t)col * ldc + pm0;
-            for (int off = 0; off < rows; off += 16)
-              asm volatile("prefetch.global.L2 [%0];\n" ::"l"(c0 + off));
-            asm volatile("prefetch.global.L2 [%0];\n" ::"l"(c0 + rows - 1));
+      // C block of the unit through CS ring slots (my_dgemm contract only:
+      // the BLAS epilogue reads C at the end instead).  The copies are issued
+      // while the consumers finish the previous unit, so the C load is off the
+      // critical path and spread in time instead of bursting at unit start.
+      if (!ep.blas) {
+        const bool c_bulk = c_aligned && (m0 + BM <= M) && (n0 + BN <= N);
+        for (int cs = 0; cs < CS; ++cs, ++g) {
+          const int slot = g % STAGES;
+          if (g >= STAGES) mbar_wait(&empty_bar[slot], ((g / STAGES) - 1) & 1);
+          double *cb = smem + slot * SLOT;
+          const int c_first = n0 + cs * CPS;
+          if (c_bulk) {
+            constexpr int CW = CPS / PRODUCER_WARPS;  // columns per producer warp
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], CW * BM * 8);
+            __syncwarp();
+            if (lane < CW) {
+              const int col = pw * CW + lane;
+              bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, BM * 8, &full_bar[slot]);
+            }
+          } else {
+            for (int idx = pw * 32 + lane; idx < CPS * BM; idx += 32 * PRODUCER_WARPS) {
+              const int col = idx / BM, row = idx % BM;
+              const bool ok = (m0 + row < M) && (c_first + col < N);
+              cp_async<8>(cb + col * CP + row, ok ? C + (int64_t)(c_first + col) * ldc + m0 + row : C, ok ? 8 : 0);
+            }
+            cp_async_mbar_arrive_inc(&full_bar[slot]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full_bar[slot]);
           }
         }
       }
@@ -207,8 +229,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           }
         }
         const int kbase = kt * BK;
-        double *as = As + slot * A_STAGE;
-        double *bs = Bs + slot * B_STAGE;
+        double *as = smem + slot * SLOT;
+        double *bs = as + A_STAGE;
         if (interior && kbase + BK <= K) {
           constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
           constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
@@ -280,15 +302,15 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   const int b_off = (wn * WN + r) * BP + q;  // + j*8*BP + kk*4
   double fa[2][FM], fb[2][FN];
   auto load_frags = [&](int buf, int slot, int kk) {
-    const double *as = As + slot * A_STAGE + a_off + kk * 4 * AP;
-    const double *bs = Bs + slot * B_STAGE + b_off + kk * 4;
+    const double *as = smem + slot * SLOT + a_off + kk * 4 * AP;
+    const double *bs = smem + slot * SLOT + A_STAGE + b_off + kk * 4;
 #pragma unroll
     for (int i = 0; i < FM; ++i) fa[buf][i] = as[i * 8];
 #pragma unroll
     for (int j = 0; j < FN; ++j) fb[buf][j] = bs[j * 8 * BP];
   };
 
-  uint32_t g = 0;  // ring position of this unit's first slab
+  uint32_t g = 0;  // ring position (C blocks and slabs consumed so far)
   for (int u = blockIdx.x; u < units; u += gridDim.x, g += KT) {
     int m0, n0;
     unit_origin(u, m0, n0);
@@ -298,29 +320,30 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #ifdef MYD_FAST_PROFILE
     long long c_t0 = clock64();
 #endif
+    if (!ep.blas) {  // the accumulator starts at C (_mk's tile load), staged in CS ring slots
+      for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(g + cs) % STAGES], ((g + cs) / STAGES) & 1);
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j)
+        for (int j = 0; j < FN; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int row = row0 + i * 8, col = col0 + j * 8 + e;
-#ifdef MYD_FAST_CLOAD_CG
-          acc[i][j][e] = (!ep.blas && row < M && col < N) ? __ldcg(C + (int64_t)col * ldc + row) : 0.0;
-#else
-          acc[i][j][e] = (!ep.blas && row < M && col < N) ? C[(int64_t)col * ldc + row] : 0.0;
-#endif
-        }
-#ifdef MYD_FAST_PROFILE
-    {  // force the C loads to land before timing the main loop
-      double sink = 0;
+          for (int e = 0; e < 2; ++e) {
+            const int cl = wn * WN + j * 8 + 2 * q + e, rl = wm * WM + i * 8 + r;
+            acc[i][j][e] = smem[((g + cl / CPS) % STAGES) * SLOT + (cl % CPS) * CP + rl];
+          }
+      __syncwarp();
+      if (lane == 0)
+        for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(g + cs) % STAGES]);
+      g += CS;
+    } else {
 #pragma unroll
-      for (int i = 0; i < FM; ++i) sink += acc[i][0][0];
-      if (sink == 1.2345e-300) acc[0][0][1] += 1;
-      if (lane == 0) PROF_ADD(6, clock64() - c_t0);
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
+#ifdef MYD_FAST_PROFILE
+    if (lane == 0) PROF_ADD(6, clock64() - c_t0);
 #endif
-
 #ifdef MYD_FAST_PROFILE
     long long loop_t0 = clock64();
 #endif
