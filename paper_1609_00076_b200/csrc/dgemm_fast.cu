@@ -95,9 +95,10 @@ struct Ring {
   static constexpr int B_ST = BN * BP;  // doubles per B slab
   static constexpr int SLOT = A_ST + B_ST;  // one ring slot: A slab then B slab
   // A unit's C block is staged through ring slots before its first slab:
-  // CPS columns per slot at pitch CP = BM + 2 (column-pair stride = 32 B mod
-  // 128, so the consumers' C fragment loads are conflict-free), CS slots.
-  static constexpr int CP = BM + 2;
+  // CPS columns per slot at pitch CP = BM + 8 (column stride = 64 B mod 128:
+  // a quarter-warp's 16-byte fragment loads of 2 columns x 64 B are
+  // conflict-free), CS slots.
+  static constexpr int CP = BM + 8;
   static constexpr int CPS = (64 <= BN && 64 * CP <= SLOT) ? 64
                              : (32 <= BN && 32 * CP <= SLOT) ? 32
                              : (16 * CP <= SLOT) ? 16 : 8;
@@ -315,8 +316,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     int m0, n0;
     unit_origin(u, m0, n0);
     double acc[FM][FN][2];
-    const int row0 = m0 + wm * WM + r;
-    const int col0 = n0 + wn * WN + 2 * q;
+    // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
+    // thread's pair is two consecutive rows of one column: 16 contiguous
+    // bytes in column-major C):  acc[i][j][e] = C(row0 + 8i + e, col0 + 8j).
+    const int row0 = m0 + wm * WM + 2 * q;
+    const int col0 = n0 + wn * WN + r;
 #ifdef MYD_FAST_PROFILE
     long long c_t0 = clock64();
 #endif
@@ -325,12 +329,13 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
-        for (int j = 0; j < FN; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int cl = wn * WN + j * 8 + 2 * q + e, rl = wm * WM + i * 8 + r;
-            acc[i][j][e] = smem[((g + cl / CPS) % STAGES) * SLOT + (cl % CPS) * CP + rl];
-          }
+        for (int j = 0; j < FN; ++j) {
+          const int cl = wn * WN + j * 8 + r, rl = wm * WM + i * 8 + 2 * q;
+          const double2 v = *reinterpret_cast<const double2 *>(
+              &smem[((g + cl / CPS) % STAGES) * SLOT + (cl % CPS) * CP + rl]);
+          acc[i][j][0] = v.x;
+          acc[i][j][1] = v.y;
+        }
       __syncwarp();
       if (lane == 0)
         for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(g + cs) % STAGES]);
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
-          for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fa[cur][i], fb[cur][j]);
+          for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fb[cur][j], fa[cur][i]);
       }
       // every fragment of this slab has been consumed by an issued DMMA
       __syncwarp();
@@ -394,21 +399,27 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     }
 #endif
     // ---- epilogue: valid region only (padding rows never touched) ----
+    const bool vec_store = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int row = row0 + i * 8, col = col0 + j * 8 + e;
-          if (row < M && col < N) {
-            double *cp = C + (int64_t)col * ldc + row;
-            if (!ep.blas)
-              *cp = acc[i][j][e];
-            else  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
-              *cp = ep.beta == 0.0 ? ep.alpha * acc[i][j][e] : fma(ep.alpha, acc[i][j][e], ep.beta * *cp);
-          }
+      for (int j = 0; j < FN; ++j) {
+        const int row = row0 + i * 8, col = col0 + j * 8;
+        if (col >= N || row >= M) continue;
+        double *cp = C + (int64_t)col * ldc + row;
+        double v0 = acc[i][j][0], v1 = acc[i][j][1];
+        const bool pair = row + 1 < M;
+        if (ep.blas) {  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
+          v0 = ep.beta == 0.0 ? ep.alpha * v0 : fma(ep.alpha, v0, ep.beta * cp[0]);
+          if (pair) v1 = ep.beta == 0.0 ? ep.alpha * v1 : fma(ep.alpha, v1, ep.beta * cp[1]);
         }
+        if (pair && vec_store) {
+          *reinterpret_cast<double2 *>(cp) = make_double2(v0, v1);
+        } else {
+          cp[0] = v0;
+          if (pair) cp[1] = v1;
+        }
+      }
   }
 }
 
