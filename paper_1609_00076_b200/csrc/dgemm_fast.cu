@@ -195,23 +195,31 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           if (g >= STAGES) mbar_wait(&empty_bar[slot], ((g / STAGES) - 1) & 1);
           double *cb = smem + slot * SLOT;
           const int c_first = n0 + cs * CPS;
-          if (c_bulk) {
-            constexpr int CW = CPS / PRODUCER_WARPS;  // columns per producer warp
-            if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], CW * BM * 8);
-            __syncwarp();
-            if (lane < CW) {
-              const int col = pw * CW + lane;
-              bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, BM * 8, &full_bar[slot]);
+          // Producer warp pw stages columns [pw*CW, pw*CW+CW) of this slot.
+          // Whole aligned columns go by bulk copy; otherwise only the valid
+          // rows of valid columns are copied (8-byte cp.async); rows/columns
+          // outside C stay stale -- their accumulators are never stored.
+          constexpr int CW = CPS / PRODUCER_WARPS;
+          const int rows = max(0, min(BM, M - m0));  // 0 for a unit wholly below C
+          const bool col_bulk = c_aligned && (rows % 2 == 0);
+          if (!c_bulk && !col_bulk) {
+            for (int c = 0; c < CW; ++c) {
+              const int col = pw * CW + c;
+              if (c_first + col >= N) break;
+              for (int row = lane; row < rows; row += 32)
+                cp_async<8>(cb + col * CP + row, C + (int64_t)(c_first + col) * ldc + m0 + row, 8);
             }
-          } else {
-            for (int idx = pw * 32 + lane; idx < CPS * BM; idx += 32 * PRODUCER_WARPS) {
-              const int col = idx / BM, row = idx % BM;
-              const bool ok = (m0 + row < M) && (c_first + col < N);
-              cp_async<8>(cb + col * CP + row, ok ? C + (int64_t)(c_first + col) * ldc + m0 + row : C, ok ? 8 : 0);
-            }
-            cp_async_mbar_arrive_inc(&full_bar[slot]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full_bar[slot]);
+          }
+          cp_async_mbar_arrive_inc(&full_bar[slot]);
+          __syncwarp();
+          int valid_cols = min(CW, N - c_first - pw * CW);
+          valid_cols = (valid_cols < 0 || rows == 0) ? 0 : valid_cols;
+          const uint32_t bulk_bytes = (c_bulk || col_bulk) ? (uint32_t)(valid_cols * rows * 8) : 0u;
+          if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], bulk_bytes);
+          __syncwarp();
+          if ((c_bulk || col_bulk) && lane < valid_cols) {
+            const int col = pw * CW + lane;
+            bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, rows * 8, &full_bar[slot]);
           }
         }
       }
