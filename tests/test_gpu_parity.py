@@ -423,3 +423,33 @@ def test_host_path_pageable_and_pinned_agree(torch_cuda, pinned):
             dc, ldc)
     assert np.array_equal(oracle.valid_region(got, m, n, ldc), oracle.valid_region(dc.cpu().numpy(), m, n, ldc))
     assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
+
+
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (1, 1, 777), (1, 5, 1), (5, 1, 1), (200, 300, 1), (2, 2, 4096)])
+def test_degenerate_shapes(torch_cuda, m, n, k):
+    check_fast_vs_oracle(m, n, k, m + 1, k + 3, m + 2)
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, m + 1, k + 3, m + 2)
+    want = oracle.naive(m, n, k, a, m + 1, b, k + 3, c.copy(), m + 2)
+    got = engine.my_dgemm(m, n, k, a, m + 1, b, k + 3, c.copy(), m + 2, exact=True)
+    assert np.array_equal(got, want)
+
+
+def test_nonfinite_propagation_matches_oracle(torch_cuda):
+    """Inf and NaN inputs give non-finite outputs exactly where the reference's
+    naive loop produces them (exact mode: bitwise including NaN positions)."""
+    m, n, k = 150, 140, 90
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, m, k, m)
+    a[5 * m + 3] = np.inf          # A(3, 5)
+    a[7 * m + 100] = -np.inf       # A(100, 7)
+    b[11 * k + 5] = np.nan         # B(5, 11)
+    c[13 * m + 20] = np.inf        # C(20, 13)
+    want = oracle.naive(m, n, k, a, m, b, k, c.copy(), m)
+    for exact in (False, True):
+        got = engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m, exact=exact)
+        assert np.array_equal(np.isnan(got), np.isnan(want)), exact
+        assert np.array_equal(np.isinf(got), np.isinf(want)), exact
+        fin = np.isfinite(want)
+        assert np.abs(got[fin] - want[fin]).max() <= oracle.tolerance(k, 1.0, 1.0)
+        if exact:
+            assert np.array_equal(got[fin], want[fin])
+            assert np.array_equal(np.signbit(got[np.isinf(got)]), np.signbit(want[np.isinf(want)]))
