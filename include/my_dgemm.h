@@ -118,6 +118,18 @@ MY_DGEMM_API uint64_t my_dgemm_operand_seed(uint64_t seed, uint64_t role, int64_
 MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
                           double tol, double *out_max, int64_t *out_first_bad, void *stream);
 
+/*
+ * CTA-plan autotuner (the GPU analogue of the reference's grid tuner,
+ * pkg/src/gemmforge/bench.py:238-311): times every launch plan of the fast
+ * kernel for this shape (heuristic, full tiles only, all 128x64 / 128x32 /
+ * 64x32 units) on scratch device operands and remembers the fastest for
+ * later calls of the same shape and operand alignment in this process.
+ * Plans are bitwise-equivalent: tuning changes speed, never results.
+ * out_plan: 0 heuristic, 1 full tiles, 2/4/8 units per tile.
+ */
+MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan, double *out_ms);
+MY_DGEMM_API void my_dgemm_tune_clear(void);
+
 /* Diagnostics. */
 MY_DGEMM_API const char *my_dgemm_last_error(void);
 MY_DGEMM_API int my_dgemm_last_status(void);

@@ -23,6 +23,7 @@ from .engine import (  # noqa: F401
     my_dgemm,
     operand_seed,
     register,
+    tune,
 )
 
 __version__ = "0.1.0"

@@ -40,6 +40,8 @@ SIGNATURES = {
     "my_dgemm_operand_seed": (_U64, [_U64, _U64, _I64, _I64, _I64]),
     "my_dgemm_max_abs_diff": (_I, [_I64, _I64, _P, _I64, _P, _I64, _D, ctypes.POINTER(_D),
                                    ctypes.POINTER(_I64), _P]),
+    "my_dgemm_tune": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_D)]),
+    "my_dgemm_tune_clear": (None, []),
     "my_dgemm_last_error": (ctypes.c_char_p, []),
     "my_dgemm_last_status": (_I, []),
     "my_dgemm_version": (ctypes.c_char_p, []),

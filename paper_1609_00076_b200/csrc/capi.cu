@@ -36,6 +36,8 @@ cudaError_t launch_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t l
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+int tuned_plan(int m, int n, int k, int64_t lda, int64_t ldb);
+
 // Device-pointer dispatch: picks the kernel for the shape.
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep) {
@@ -44,10 +46,11 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     if (n == 1) return launch_gemv_n1(m, k, A, lda, B, C, st, ep);
     if (m == 1) return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st, ep);
   }
-  const int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
-                    : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
-                    : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
-                                                       : 0;
+  int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
+              : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
+              : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
+                                                 : 0;
+  if (split == 0) split = tuned_plan(m, n, k, lda, ldb);  // 0 unless my_dgemm_tune chose one
   return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, (flags & MY_DGEMM_FORCE_VEC1) != 0, split, ep);
 }
 

@@ -499,7 +499,8 @@ int sm_count() {
 // into `split` units (128x64, 128x32 or 64x32; all 8 consumer warps busy)
 // when that shortens the last wave, whose cost is ceil(r*split/G)/split
 // tile-times.  Small problems (q = 0) therefore run entirely as small units.
-// force_split (0 = plan) pins the unit shape for tests.
+// force_split pins the plan (tests and the tuner): 0 = heuristic above,
+// 1 = full tiles only (no tail re-cut), 2 / 4 / 8 = every tile as units.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -516,6 +517,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     split = force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2);  // every tile as units
     q = 0;
     r = tiles;
+  } else if (force_split == 1) {
+    split = 1;
   } else if (r > 0) {
     double best = 1.0;
     for (int s : {2, 4, 8}) {

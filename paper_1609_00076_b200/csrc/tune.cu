@@ -1,0 +1,116 @@
+// tune.cu -- the CTA-plan autotuner (the GPU analogue of
+// the reference's grid tuner, pkg/src/gemmforge/bench.py:238-311).
+//
+// For one shape it times every launch plan of the fast kernel -- the
+// heuristic plan, full tiles only, and every tile as 128x64 / 128x32 / 64x32
+// units -- on device operands, keeps the fastest in a per-process table keyed
+// by (device, m, n, k, operand alignment), and later calls of that shape use
+// it.  Every plan computes bitwise the same C (the per-element DMMA sequence
+// does not depend on the unit shape), so tuning can change speed, never
+// results.
+#include <map>
+#include <string>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/my_dgemm.h"
+#include "common.cuh"
+
+namespace myd {
+
+cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                              double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
+                              const Epilogue &ep);
+cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
+                               cudaStream_t stream);
+int capi_fail(int status, const std::string &msg);
+int capi_ok();
+int capi_cuda_fail(cudaError_t e, const char *where);
+
+namespace {
+using Key = std::tuple<int, int, int, int, bool, bool>;  // device, m, n, k, lda even, ldb even
+std::mutex g_tune_mu;
+std::map<Key, int> g_tuned;
+
+Key make_key(int m, int n, int k, int64_t lda, int64_t ldb) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return Key{dev, m, n, k, lda % 2 == 0, ldb % 2 == 0};
+}
+}  // namespace
+
+int tuned_plan(int m, int n, int k, int64_t lda, int64_t ldb) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  if (g_tuned.empty()) return 0;
+  auto it = g_tuned.find(make_key(m, n, k, lda, ldb));
+  return it == g_tuned.end() ? 0 : it->second;
+}
+
+}  // namespace myd
+
+using namespace myd;
+
+extern "C" int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan,
+                             double *out_ms) {
+  if (m < 1) return capi_fail(-1, "matrix dims must be positive");
+  if (n < 1) return capi_fail(-2, "matrix dims must be positive");
+  if (k < 1) return capi_fail(-3, "matrix dims must be positive");
+  if (lda < m) return capi_fail(-4, "leading dimension lda smaller than m");
+  if (ldb < k) return capi_fail(-5, "leading dimension ldb smaller than k");
+  if (ldc < m) return capi_fail(-6, "leading dimension ldc smaller than m");
+  if (reps < 1) reps = 3;
+  cudaStream_t st = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return capi_cuda_fail(e, "cudaStreamCreate");
+  double *A = nullptr, *B = nullptr, *C = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int best_plan = 0;
+  float best = -1.f;
+  do {
+    if ((e = cudaMallocAsync((void **)&A, (size_t)lda * k * 8, st)) != cudaSuccess) break;
+    if ((e = cudaMallocAsync((void **)&B, (size_t)ldb * n * 8, st)) != cudaSuccess) break;
+    if ((e = cudaMallocAsync((void **)&C, (size_t)ldc * n * 8, st)) != cudaSuccess) break;
+    if ((e = launch_fill_random(A, m, k, lda, 1, 0, st)) != cudaSuccess) break;
+    if ((e = launch_fill_random(B, k, n, ldb, 2, 0, st)) != cudaSuccess) break;
+    if ((e = launch_fill_random(C, m, n, ldc, 3, 0, st)) != cudaSuccess) break;
+    if ((e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess) break;
+    const int plans[] = {0, 1, 2, 4, 8};
+    for (int plan : plans) {
+      const Epilogue ep{};
+      if ((e = launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, false, plan, ep)) != cudaSuccess) break;
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < reps && e == cudaSuccess; ++r)
+        e = launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, false, plan, ep);
+      if (e != cudaSuccess) break;
+      cudaEventRecord(e1, st);
+      if ((e = cudaEventSynchronize(e1)) != cudaSuccess) break;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ms /= reps;
+      if (best < 0.f || ms < best * 0.99f) {  // prefer the earlier (heuristic) plan on near-ties
+        best = ms;
+        best_plan = plan;
+      }
+    }
+  } while (false);
+  if (A) cudaFreeAsync(A, st);
+  if (B) cudaFreeAsync(B, st);
+  if (C) cudaFreeAsync(C, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (e != cudaSuccess) return capi_cuda_fail(e, "tune");
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned[make_key(m, n, k, lda, ldb)] = best_plan;
+  }
+  if (out_plan) *out_plan = best_plan;
+  if (out_ms) *out_ms = best;
+  return capi_ok();
+}
+
+extern "C" void my_dgemm_tune_clear(void) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tuned.clear();
+}

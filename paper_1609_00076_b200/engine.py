@@ -47,6 +47,7 @@ __all__ = [
     "max_abs_diff_device",
     "kernel_launches",
     "dgemm",
+    "tune",
 ]
 
 
@@ -271,3 +272,15 @@ def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A, lda
                            ctypes.c_void_p(stream) if dev else None)
     _capi.check(st)
     return C
+
+
+def tune(m: int, n: int, k: int, lda: int | None = None, ldb: int | None = None, ldc: int | None = None,
+         reps: int = 3) -> tuple[int, float]:
+    """Pick the fastest launch plan for this shape (my_dgemm_tune); later calls
+    of the shape use it.  Returns (plan, ms).  Results are unaffected."""
+    lib = _capi.load()
+    plan = ctypes.c_int()
+    ms = ctypes.c_double()
+    _capi.check(lib.my_dgemm_tune(m, n, k, lda or m, ldb or k, ldc or m, reps, ctypes.byref(plan),
+                                  ctypes.byref(ms)))
+    return plan.value, ms.value

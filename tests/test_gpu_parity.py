@@ -453,3 +453,16 @@ def test_nonfinite_propagation_matches_oracle(torch_cuda):
         if exact:
             assert np.array_equal(got[fin], want[fin])
             assert np.array_equal(np.signbit(got[np.isinf(got)]), np.signbit(want[np.isinf(want)]))
+
+
+def test_tuner_changes_speed_never_results(torch_cuda):
+    m, n, k = 1792, 1792, 600
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    c1 = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, c1, m)
+    plan, ms = engine.tune(m, n, k)
+    assert plan in (0, 1, 2, 4, 8) and ms > 0
+    c2 = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, c2, m)
+    assert torch_cuda.equal(c1, c2)
+    _capi.load().my_dgemm_tune_clear()
