@@ -520,15 +520,25 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   } else if (force_split == 1) {
     split = 1;
   } else if (r > 0) {
-    double best = 1.0;
+    // Cost in full-tile times, smaller units discounted by their measured
+    // efficiency (per-slab overhead grows as the unit shrinks):
+    //   full tiles + leftovers as s-units : q + ceil(r s / G) / (s eff_s)
+    //   every tile as 64x32 units         : ceil(8 T / G) / (8 eff_8)
+    auto eff = [](int s) { return s == 2 ? 0.97 : (s == 4 ? 0.95 : 0.92); };
+    double best = 1.0;  // leftovers as full tiles: one more round
     for (int s : {2, 4, 8}) {
-      // 64-high units only pay off when they fill otherwise idle SMs
-      if (s == 8 && q > 0) continue;
-      const double cost = (double)((r * s + G - 1) / G) / s;
+      if (s == 8 && q > 0) continue;  // 64-high tail units only when nothing else runs
+      const double cost = (double)((r * s + G - 1) / G) / s / eff(s);
       if (cost < best - 1e-9) {
         best = cost;
         split = s;
       }
+    }
+    const double all8 = (double)((tiles * 8 + G - 1) / G) / 8 / eff(8);
+    if (q > 0 && all8 < (double)q + best - 1e-9) {  // e.g. 1792^3: 196 tiles on 148 SMs
+      split = 8;
+      q = 0;
+      r = tiles;
     }
   }
   const long long main_tiles = split == 1 ? tiles : q * G;

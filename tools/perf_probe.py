@@ -1,5 +1,7 @@
 """Quick device-resident timing probe of the fast kernel (development aid)."""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1609_00076_b200 import engine
 
