@@ -25,6 +25,7 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
 int capi_fail(int status, const std::string &msg);
 int capi_ok();
 int capi_cuda_fail(cudaError_t e, const char *where);
+void keep_pool_memory();
 
 // dst (cols x rows, ld ldd) = src^T (src: rows x cols, ld lds); 32x32 tiles.
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
@@ -81,6 +82,7 @@ static int blas_device(char ta, char tb, int m, int n, int k, double alpha, cons
     return e == cudaSuccess ? capi_ok() : capi_cuda_fail(e, "scale");
   }
   const bool tA = is_trans(ta), tB = is_trans(tb);
+  if (tA || tB) keep_pool_memory();
   const int64_t ldA = ((int64_t)m + 1) & ~1LL, ldB = ((int64_t)k + 1) & ~1LL;
   double *wa = nullptr, *wb = nullptr;
   const double *opA = A, *opB = B;
@@ -153,6 +155,7 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
 
   // Host operands: stage through stream-ordered device buffers (pitched
   // copies never touch padding rows), run on the device, copy C back.
+  keep_pool_memory();
   cudaStream_t st = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e != cudaSuccess) return capi_cuda_fail(e, "cudaStreamCreate");

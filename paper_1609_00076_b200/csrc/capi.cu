@@ -30,6 +30,8 @@ cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const dou
                            int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
                                cudaStream_t stream);
+cudaError_t launch_copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+                          cudaStream_t stream);
 cudaError_t launch_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
                                 double tol, unsigned long long *d_out2, cudaStream_t stream);
 
@@ -37,6 +39,24 @@ static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
 int tuned_plan(int m, int n, int k, int64_t lda, int64_t ldb);
+
+// Stream-ordered scratch (odd-ld copies, BLAS transposes) comes from the
+// device's default memory pool; keep its memory instead of returning it to
+// the OS at every synchronisation, so repeated calls do not re-map pages.
+void keep_pool_memory() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done.fetch_or(bit, std::memory_order_release);
+}
 
 // Device-pointer dispatch: picks the kernel for the shape.
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
@@ -51,7 +71,51 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
               : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
                                                  : 0;
   if (split == 0) split = tuned_plan(m, n, k, lda, ldb);  // 0 unless my_dgemm_tune chose one
-  return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, (flags & MY_DGEMM_FORCE_VEC1) != 0, split, ep);
+  const bool force_vec1 = (flags & MY_DGEMM_FORCE_VEC1) != 0;
+  const bool a_ok = lda % 2 == 0 && (uintptr_t)A % 16 == 0, b_ok = ldb % 2 == 0 && (uintptr_t)B % 16 == 0;
+  const bool c_ok = ldc % 2 == 0 && (uintptr_t)C % 16 == 0;
+  if (!force_vec1 && (!a_ok || !b_ok || !c_ok) && (double)m * n * k >= (double)(1 << 24)) {
+    keep_pool_memory();
+    // Odd leading dimension (or 8-byte aligned view): copy the operand once
+    // into an even-ld scratch copy so the bulk-copy staging and 16-byte C
+    // accesses apply (C is copied back, valid rows only).  Each copy costs
+    // 16 bytes per element against 2mnk flops (a few % for m, n, k >= 1000);
+    // the arithmetic, hence C, is bitwise unchanged.
+    double *wa = nullptr, *wb = nullptr, *wc = nullptr;
+    const double *a2 = A, *b2 = B;
+    double *c2 = C;
+    int64_t lda2 = lda, ldb2 = ldb, ldc2 = ldc;
+    bool ok = true;
+    if (!a_ok) {
+      lda2 = ((int64_t)m + 1) & ~1LL;
+      ok = cudaMallocAsync((void **)&wa, (size_t)lda2 * k * 8, st) == cudaSuccess &&
+           launch_copy2d(m, k, A, lda, wa, lda2, st) == cudaSuccess;
+      a2 = wa;
+    }
+    if (ok && !b_ok) {
+      ldb2 = ((int64_t)k + 1) & ~1LL;
+      ok = cudaMallocAsync((void **)&wb, (size_t)ldb2 * n * 8, st) == cudaSuccess &&
+           launch_copy2d(k, n, B, ldb, wb, ldb2, st) == cudaSuccess;
+      b2 = wb;
+    }
+    if (ok && !c_ok) {
+      ldc2 = ((int64_t)m + 1) & ~1LL;
+      ok = cudaMallocAsync((void **)&wc, (size_t)ldc2 * n * 8, st) == cudaSuccess &&
+           ((ep.blas && ep.beta == 0.0) ||  // C is not read: nothing to copy in
+            launch_copy2d(m, n, C, ldc, wc, ldc2, st) == cudaSuccess);
+      c2 = wc;
+    }
+    cudaError_t e = cudaSuccess;
+    if (ok) e = launch_dgemm_fast(m, n, k, a2, lda2, b2, ldb2, c2, ldc2, st, false, split, ep);
+    if (ok && e == cudaSuccess && wc)
+      e = launch_copy2d(m, n, wc, ldc2, C, ldc, st);
+    if (wa) cudaFreeAsync(wa, st);
+    if (wb) cudaFreeAsync(wb, st);
+    if (wc) cudaFreeAsync(wc, st);
+    if (ok) return e;
+    cudaGetLastError();  // scratch unavailable: fall through to 8-byte staging
+  }
+  return launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, force_vec1, split, ep);
 }
 
 }  // namespace myd

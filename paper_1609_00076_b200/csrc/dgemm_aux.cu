@@ -130,6 +130,29 @@ cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, ui
 }
 
 // ---------------------------------------------------------------------------
+// Pitched device copy of the valid rows x cols block (8-byte elements, any
+// alignment): the odd-leading-dimension pre/post pass of the fast path.
+// (cudaMemcpy2D between pitches that are not multiples of 16 bytes runs at a
+// fraction of HBM bandwidth.)  Grid-stride over columns, rows coalesced.
+// ---------------------------------------------------------------------------
+__global__ void copy2d_kernel(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
+                              double *__restrict__ dst, int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+      dst[j * ldd + i] = __ldcs(src + j * lds + i);
+}
+
+cudaError_t launch_copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
+                          cudaStream_t stream) {
+  const int threads = 256;
+  const int64_t gx = std::min<int64_t>((rows + threads - 1) / threads, 16);
+  const int64_t gy = std::min<int64_t>(cols, 65535);
+  copy2d_kernel<<<dim3((unsigned)gx, (unsigned)gy), threads, 0, stream>>>(rows, cols, src, lds, dst, ldd);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // max_abs_diff (matrix.py:210-232): max |X-Y| over the valid region and the
 // first flat index t = j*m + i with |X-Y| > tol (NaN counts as bad).  Max and
 // min are order-independent, so atomics keep the answer deterministic.

@@ -466,3 +466,20 @@ def test_tuner_changes_speed_never_results(torch_cuda):
     run_dev(torch_cuda, m, n, k, a, m, b, k, c2, m)
     assert torch_cuda.equal(c1, c2)
     _capi.load().my_dgemm_tune_clear()
+
+
+def test_odd_ld_prepass_bitwise_equals_aligned(torch_cuda):
+    """Odd leading dimensions take the even-ld scratch copy path (A, B and C):
+    bitwise the same C as the same operands stored with even leading
+    dimensions, and padding rows of C untouched."""
+    m, n, k = 1001, 1203, 777
+    odd = dev_operands(torch_cuda, m, n, k, 1003, 781, 1005, canary=-777.25)
+    even = dev_operands(torch_cuda, m, n, k, 1002, 778, 1004, canary=-777.25)
+    a, b, c, (lda, ldb, ldc) = odd
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    a2, b2, c2, (lda2, ldb2, ldc2) = even
+    run_dev(torch_cuda, m, n, k, a2, lda2, b2, ldb2, c2, ldc2)
+    g1 = oracle.valid_region(c.cpu().numpy(), m, n, ldc)
+    g2 = oracle.valid_region(c2.cpu().numpy(), m, n, ldc2)
+    assert np.array_equal(g1, g2)
+    assert np.all(c.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
