@@ -2,30 +2,31 @@
 //
 // The reference's five BLIS loops (pkg/src/gemmforge/goto.py:187-239 and
 // _ckernels.pyx:15-45,142-195) re-derived for Blackwell:
-//   loop 5/3 (jc, ic)  -> the CTA grid over 128x128 tiles of C, rastered in
-//                         bands of GROUP_M tile-rows so co-resident CTAs share
-//                         A and B panels in the 126 MB L2; the last partial
-//                         wave is re-cut into 128x64 / 128x32 strips so every
-//                         SM gets work (launch_dgemm_fast);
-//   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs (16 for full tiles);
-//   pack_a / pack_b    -> producer warps stage each A and B slab into a
-//                         multi-stage shared-memory ring: bulk copies by the
-//                         TMA engine (cp.async.bulk, one per A k-row and per
-//                         B column segment) for interior tiles, zero-filling
-//                         cp.async (LDGSTS) at the edges; no pack pass touches
-//                         HBM;
+//   loop 5/3 (jc, ic)  -> persistent CTAs (one per SM) walking 128x128 units of
+//                         C round-robin, rastered in bands of GROUP_M tile-rows
+//                         so co-resident CTAs share A and B panels in the
+//                         126 MB L2; the last partial wave (or a small
+//                         problem) is re-cut into 128x64 / 128x32 / 64x32
+//                         units so every SM gets work (launch_dgemm_fast);
+//   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs;
+//   pack_a / pack_b    -> producer warps stage each A and B slab (and, first,
+//                         the unit's C block) into a multi-stage shared-memory
+//                         ring: bulk copies by the TMA engine (cp.async.bulk)
+//                         for aligned interior data, zero-filling cp.async
+//                         (LDGSTS) at the edges; no pack pass touches HBM;
 //   loops 2/1 + _mk    -> 8 consumer warps, each a register tile of C built
 //                         from DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
 //                         no tcgen05 kind on sm_100a; the DMMA pipe measured
 //                         37.1 TFLOP/s (128 flop/clk/SM) vs 34.0 for DFMA
 //                         (profiles/fp64_peak_r01.txt).
-// C is loaded into the accumulators first, like _mk's tile load
-// (_ckernels.pyx:28-32), and only the valid region is stored back.
+// The accumulators start from C, like _mk's tile load (_ckernels.pyx:28-32),
+// and only the valid region is stored back.  The DMMA computes the C^T block
+// (B^T A^T) so each thread's accumulator pair is 16 contiguous bytes of C.
 //
 // Per-element arithmetic (k grouped in fours from p = 0, one DMMA per group,
 // groups in ascending order, accumulator starting at C) does not depend on
-// the CTA width, the tile position or the launch plan, so every plan and
-// every k-chunking at multiples of 16 gives bitwise the same C.
+// the unit shape, the tile position, the K-slab depth or the launch plan, so
+// every plan and every k-chunking at multiples of 16 gives bitwise the same C.
 #include <algorithm>
 #include <atomic>
 #include <type_traits>
@@ -68,19 +69,17 @@ constexpr int THREADS = (CONSUMER_WARPS + PRODUCER_WARPS) * 32;
 constexpr int PRODUCER_REGS = 40;
 constexpr int CONSUMER_REGS = 232;
 constexpr int WN = 32;  // warp tile width (4 DMMA column fragments)
-// Padded pitches make every fragment load and every 16-byte staging store
-// conflict-free: a half-warp's 4 k-rows of A (4 n-rows of B) land in 4
-// distinct 32-byte bank groups (pitch = 4 mod 16 doubles).
 // Ring geometry per CTA shape.  The K slab grows as the unit shrinks so
 // every consumer warp still issues >= 64 DMMAs per slab (the per-slab
 // barrier probe and release cost ~200 cycles): 16 for 128x128 / 128x64,
 // 32 for 128x32, 64 for 64x32; full tiles of long-K aligned problems use 32
 // (3 stages: fewer probes, 97.4 % vs 96.4 % at 8192^3) while short-K ones
-// keep 16 (5 stages: deeper prefetch across unit boundaries, cfg4 89.6 %
-// vs 84 %).  As many stages as fit the budget.
-// Pitches are 4 mod 16 doubles so fragment loads and 16-byte staging
-// stores are bank-conflict free: A slab [BK][BM+4] (m contiguous, as in
-// HBM), B slab [BN][BK+4] (k contiguous, as in HBM).
+// keep 16 (6 stages: deeper prefetch across unit boundaries, cfg4 89 % vs
+// 84 %).  As many stages as fit the budget.  Pitches are 4 mod 16 doubles,
+// so a half-warp's 4 k-rows of A (4 n-rows of B) land in 4 distinct 32-byte
+// bank groups and every fragment load and 16-byte staging store is
+// conflict-free: A slab [BK][BM+4] (m contiguous, as in HBM), B slab
+// [BN][BK+4] (k contiguous, as in HBM).
 template <int BM, int BN>
 constexpr int default_bk() {
   return (BM * BN) / (CONSUMER_WARPS * 64) >= 16 ? 16 : ((BM * BN) / (CONSUMER_WARPS * 64) >= 8 ? 32 : 64);
@@ -114,10 +113,11 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 }  // namespace fast
 
 // VEC: doubles per LDGSTS (2: 16-byte copies and the bulk path, needs even
-// ld and 16-B aligned bases; 1: 8-byte copies for odd ld / 8-B aligned views).
-// BN: CTA width (128 full tiles; 64 / 32 tail strips).  Warps tile the CTA as
-// (8 / (BN/32)) x (BN/32) with 32-column warp tiles, so all 8 consumer warps
-// work whatever the width.
+// ld and 16-B aligned bases; 1: 8-byte copies for odd ld / 8-B aligned views
+// -- dispatch() normally copies such operands to even-ld scratch first).
+// BM x BN: unit shape (128x128 full tiles; 128x64, 128x32, 64x32 units).
+// Warps tile the unit as (8 / (BN/32)) x (BN/32) with 32-column warp tiles, so
+// all 8 consumer warps work whatever the shape.  BKT: K-slab depth.
 //
 // Warp roles: warps 0..7 consume (DMMA), warps 8..11 produce (staging).
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
