@@ -195,6 +195,19 @@ int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, 
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8;
   if (flags & ~known) return fail(-10, "unknown flag bits");
   if (flags & MY_DGEMM_DEVICE_PTRS) {
+    // A host pointer here would fault the GPU; reject it as an argument error.
+    const void *ptrs[3] = {A, B, C};
+    for (int i = 0; i < 3; ++i) {
+      cudaPointerAttributes at;
+      const bool dev_ok = cudaPointerGetAttributes(&at, ptrs[i]) == cudaSuccess &&
+                          (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+      if (!dev_ok) {
+        cudaGetLastError();
+        const int which[3] = {-4, -6, -8};
+        return fail(which[i], std::string(i == 0 ? "A" : (i == 1 ? "B" : "C")) +
+                                  " is not a device pointer (MY_DGEMM_DEVICE_PTRS)");
+      }
+    }
     cudaError_t e = dispatch(m, n, k, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, flags);
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
     return ok();

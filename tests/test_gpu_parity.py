@@ -483,3 +483,38 @@ def test_odd_ld_prepass_bitwise_equals_aligned(torch_cuda):
     g2 = oracle.valid_region(c2.cpu().numpy(), m, n, ldc2)
     assert np.array_equal(g1, g2)
     assert np.all(c.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
+
+
+def test_device_flag_rejects_host_pointers(torch_cuda):
+    a = np.ones(16)
+    d = torch_cuda.ones(16, dtype=torch_cuda.float64, device="cuda")
+    lib = _capi.load()
+    st = lib.my_dgemm_ex(4, 4, 4, a.ctypes.data, 4, d.data_ptr(), 4, d.data_ptr(), 4, _capi.DEVICE_PTRS, None)
+    assert st == -4 and "device pointer" in _capi.last_error()
+    st = lib.my_dgemm_ex(4, 4, 4, d.data_ptr(), 4, d.data_ptr(), 4, a.ctypes.data, 4, _capi.DEVICE_PTRS, None)
+    assert st == -8
+
+
+def test_cuda_graph_capture_and_replay(torch_cuda):
+    """The device path is capture-safe: a CUDA graph of several my_dgemm_ex
+    calls replays to the same result as eager calls (launch-bound small
+    problems can be replayed without per-call host overhead)."""
+    torch = torch_cuda
+    m, n, k = 300, 257, 129
+    a, b, c, _ = dev_operands(torch, m, n, k)
+    eager = c.clone()
+    for _ in range(3):
+        run_dev(torch, m, n, k, a, m, b, k, eager, m)
+    graphed = c.clone()
+    s = torch.cuda.Stream()
+    engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, graphed.data_ptr(), m, s.cuda_stream)  # warm
+    torch.cuda.synchronize()
+    graphed.copy_(c)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(3):
+            engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, graphed.data_ptr(), m,
+                                torch.cuda.current_stream().cuda_stream)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(graphed, eager)
