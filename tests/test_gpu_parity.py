@@ -468,12 +468,14 @@ def test_tuner_changes_speed_never_results(torch_cuda):
     _capi.load().my_dgemm_tune_clear()
 
 
-def test_odd_ld_prepass_bitwise_equals_aligned(torch_cuda):
-    """Odd leading dimensions take the even-ld scratch copy path (A, B and C):
+@pytest.mark.parametrize("odd_lds", [(1003, 781, 1005), (1002, 778, 1005), (1003, 778, 1004)])
+def test_odd_ld_prepass_bitwise_equals_aligned(torch_cuda, odd_lds):
+    """Odd leading dimensions of A / B take the even-ld scratch copy path, an
+    odd ldc is read and written in place (8-byte staging, scalar stores):
     bitwise the same C as the same operands stored with even leading
     dimensions, and padding rows of C untouched."""
     m, n, k = 1001, 1203, 777
-    odd = dev_operands(torch_cuda, m, n, k, 1003, 781, 1005, canary=-777.25)
+    odd = dev_operands(torch_cuda, m, n, k, *odd_lds, canary=-777.25)
     even = dev_operands(torch_cuda, m, n, k, 1002, 778, 1004, canary=-777.25)
     a, b, c, (lda, ldb, ldc) = odd
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
@@ -483,6 +485,46 @@ def test_odd_ld_prepass_bitwise_equals_aligned(torch_cuda):
     g2 = oracle.valid_region(c2.cpu().numpy(), m, n, ldc2)
     assert np.array_equal(g1, g2)
     assert np.all(c.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
+
+
+def test_c_view_8_byte_aligned_in_place(torch_cuda):
+    """C as a view starting one double into its buffer (8-byte aligned base,
+    even ldc): staged and stored in place, bitwise the aligned result, the
+    doubles around the view untouched."""
+    m, n, k = 1030, 517, 640
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    want = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, want, m)
+    buf = torch_cuda.full((m * n + 2,), -5.5, dtype=torch_cuda.float64, device="cuda")
+    buf[1:1 + m * n].copy_(c)
+    engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, buf.data_ptr() + 8, m,
+                        torch_cuda.cuda.current_stream().cuda_stream)
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(buf[1:1 + m * n], want)
+    assert float(buf[0]) == -5.5 and float(buf[-1]) == -5.5
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_step_every_world_size_bitwise_equals_single_call(torch_cuda, world):
+    """multi.ShardedDgemm's per-rank work for world sizes 2, 3, 8 run one rank
+    after another on this GPU (A already resident: the broadcast is the
+    identity here, no rank waits on another), C panels assembled: bitwise the
+    single-GPU call.  The NCCL path then only moves A (tests/test_multi.py
+    covers the exchange with gloo)."""
+    from paper_1609_00076_b200.multi import ShardedDgemm, make_shard_plan
+
+    m, n, k = 700, 1111, 900
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    want = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, want, m, force_tiled=True)
+    got = c.clone()
+    plan = make_shard_plan(m, n, k, world, root=0, k_chunk=256)
+    for rank in range(world):
+        j0, j1 = plan.local(rank)
+        drv = ShardedDgemm(plan, rank, broadcast=lambda t, src: None)
+        drv.step(a, m, b[j0 * k:], k, got[j0 * m:], m, broadcast_a=False)
+    torch_cuda.cuda.synchronize()
+    assert torch_cuda.equal(got, want)
 
 
 def test_device_flag_rejects_host_pointers(torch_cuda):
