@@ -97,6 +97,29 @@ MY_DGEMM_API int my_dgemm_shard(int m, int nloc, int kc, const double *A, int ld
                    void *stream);
 
 /*
+ * Host-pointer my_dgemm spread over the GPUs 0..ngpu-1 of this process
+ * (SURVEY.md 8b `my_dgemm_multi(int ngpu, ...)`; the reference's threaded
+ * driver pkg/src/gemmforge/parallel.py:108-243 split over devices instead of
+ * cores).  Device g owns the balanced column panel g of B and C
+ * (128-column units); A's k-chunks are uploaded round-robin over the
+ * devices' PCIe links and copied peer to peer.  C is bitwise the
+ * single-device my_dgemm result for every ngpu.  Status: -1 bad ngpu (< 1
+ * or more than the visible devices), -2..-10 as my_dgemm_ex's -1..-9.
+ */
+MY_DGEMM_API int my_dgemm_multi(int ngpu, int m, int n, int k, const double *A, int lda, const double *B, int ldb,
+                                double *C, int ldc);
+
+/*
+ * my_dgemm_multi on an explicit device list (shard s on devices[s]; an entry
+ * may repeat -- each entry is an independent shard with its own buffers,
+ * which is how the multi-device logic is exercised on one GPU).  flags: 0 or
+ * MY_DGEMM_EXACT.  Status: -1 devices NULL, -2 bad ndev / device id,
+ * -3..-11 as my_dgemm_ex's -1..-9, -12 unknown flags.
+ */
+MY_DGEMM_API int my_dgemm_multi_ex(const int *devices, int ndev, int m, int n, int k, const double *A, int lda,
+                                   const double *B, int ldb, double *C, int ldc, unsigned flags);
+
+/*
  * Device-side splitmix64-v1 operand fill: element (i, j) of the m x n matrix
  * at `dev` (leading dimension ld) takes stream position t = (col0 + j)*m + i,
  * i.e. exactly pkg/src/gemmforge/matrix.py:184-207 (`random_values`,

@@ -36,6 +36,8 @@ SIGNATURES = {
     "my_dgemm_shard": (_I, [_I, _I, _I, _P, _I, _P, _I, _P, _I, _P]),
     "my_dgemm_blas": (_I, [ctypes.c_char, ctypes.c_char, _I, _I, _I, _D, _P, _I, _P, _I, _D, _P, _I,
                            ctypes.c_uint, _P]),
+    "my_dgemm_multi": (_I, [_I, _I, _I, _I, _P, _I, _P, _I, _P, _I]),
+    "my_dgemm_multi_ex": (_I, [ctypes.POINTER(_I), _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, ctypes.c_uint]),
     "my_dgemm_fill_random": (_I, [_P, _I64, _I64, _I64, _U64, _I64, _P]),
     "my_dgemm_operand_seed": (_U64, [_U64, _U64, _I64, _I64, _I64]),
     "my_dgemm_max_abs_diff": (_I, [_I64, _I64, _P, _I64, _P, _I64, _D, ctypes.POINTER(_D),

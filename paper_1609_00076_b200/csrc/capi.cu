@@ -6,6 +6,7 @@
 // device workspace with pitched copies (width m*8, pitch ld*8), so padding
 // rows are never read or written and nothing past (n-1)*ld+m is touched
 // (matrix.py:5-6,42-45,58-61).  The host path lives in host_path.cu.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -160,6 +161,15 @@ int validate(int m, int n, int k, const void *A, int lda, const void *B, int ldb
   return 0;
 }
 
+int visible_devices() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    count = 0;
+  }
+  return count;
+}
+
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags) {
   return myd::dispatch(m, n, k, A, lda, B, ldb, C, ldc, st, flags, Epilogue{});
@@ -171,6 +181,9 @@ namespace myd {
 int host_path(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc,
               unsigned flags);
 void release_host_workspace();
+void release_multi_workspace();
+int multi_host_path(const int *devices, int G, int m, int n, int k, const double *A, int lda, const double *B,
+                    int ldb, double *C, int ldc, unsigned flags);
 int capi_fail(int status, const std::string &msg) { return fail(status, msg); }
 int capi_ok() { return ok(); }
 int capi_cuda_fail(cudaError_t e, const char *where) { return cuda_fail(e, where); }
@@ -276,6 +289,37 @@ int my_dgemm_last_status(void) { return t_status; }
 const char *my_dgemm_version(void) { return "paper_1609_00076_b200 0.1.0 sm_100a dmma"; }
 uint64_t my_dgemm_kernel_launches(void) { return g_launches.load(); }
 
-void my_dgemm_release_workspace(void) { myd::release_host_workspace(); }
+void my_dgemm_release_workspace(void) {
+  myd::release_host_workspace();
+  myd::release_multi_workspace();
+}
+
+int my_dgemm_multi_ex(const int *devices, int ndev, int m, int n, int k, const double *A, int lda, const double *B,
+                      int ldb, double *C, int ldc, unsigned flags) {
+  if (!devices) return fail(-1, "devices is NULL");
+  if (ndev < 1 || ndev > 64) return fail(-2, "ndev must be in 1..64, got " + std::to_string(ndev));
+  int v = validate(m, n, k, A, lda, B, ldb, C, ldc);
+  if (v) return fail(v - 2, t_error);
+  if (flags & ~MY_DGEMM_EXACT) return fail(-12, "unknown flag bits (my_dgemm_multi_ex takes 0 or MY_DGEMM_EXACT)");
+  const int count = visible_devices();
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= count)
+      return fail(-2, "device id " + std::to_string(devices[i]) + " not visible (" + std::to_string(count) +
+                          " devices)");
+  return myd::multi_host_path(devices, ndev, m, n, k, A, lda, B, ldb, C, ldc, flags);
+}
+
+int my_dgemm_multi(int ngpu, int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C,
+                   int ldc) {
+  if (ngpu < 1 || ngpu > 64) return fail(-1, "ngpu must be in 1..64, got " + std::to_string(ngpu));
+  int v = validate(m, n, k, A, lda, B, ldb, C, ldc);
+  if (v) return fail(v - 1, t_error);
+  const int count = visible_devices();
+  if (ngpu > count)
+    return fail(-1, "ngpu=" + std::to_string(ngpu) + " but " + std::to_string(count) + " devices are visible");
+  int devs[64];
+  for (int i = 0; i < ngpu; ++i) devs[i] = i;
+  return myd::multi_host_path(devs, ngpu, m, n, k, A, lda, B, ldb, C, ldc, 0u);
+}
 
 }  // extern "C"

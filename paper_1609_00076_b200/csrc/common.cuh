@@ -87,6 +87,21 @@ MYD_DEVICE void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, u
       : "memory");
 }
 
+// Bulk (TMA-engine) copy shared -> global, tracked in this thread's bulk
+// group; same alignment rules.  Generic-proxy writes to the source must be
+// made visible first (fence_proxy_async_smem by the writing threads).
+MYD_DEVICE void bulk_s2g(void *gmem_dst, const void *smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem_dst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+MYD_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// Wait until this thread's bulk groups have finished READING shared memory.
+MYD_DEVICE void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+// Wait until this thread's bulk groups have completed (global writes done).
+MYD_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+MYD_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 MYD_DEVICE void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n"

@@ -35,6 +35,27 @@
 
 namespace myd {
 
+#ifdef MYD_TIMELINE
+// globaltimer (ns): [0] min CTA entry, [1] max CTA exit, CTA 0 / consumer warp 0:
+// [2] after barrier init, [3] C block ready, [4] first slab ready, [5] main loop
+// done, [6] epilogue stores issued (first unit)
+__device__ unsigned long long g_tl[32];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_MARK(i)                                                     \
+  do {                                                                 \
+    if (blockIdx.x == 0 && tid == 0) {                                 \
+      const unsigned long long _t = gtimer();                          \
+      if (unit_ord == 0) g_tl[i] = _t;                                 \
+      if (i >= 3 && unit_ord < 4) g_tl[16 + unit_ord * 4 + (i - 3)] = _t; \
+    }                                                                  \
+  } while (0)
+#else
+#define TL_MARK(i) do { } while (0)
+#endif
 #ifdef MYD_FAST_PROFILE
 // [0] consumer slow-wait cycles, [1] consumer slow waits, [2] producer empty-wait cycles,
 // [3] producer waits, [4] consumer first-slab wait cycles, [5] consumer total loop cycles,
@@ -164,6 +185,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int KT = (K + BK - 1) / BK;
+#ifdef MYD_TIMELINE
+  int unit_ord = 0;
+  if (tid == 0) atomicMin(&g_tl[0], gtimer());
+#endif
 
   if (tid == 0) {
 #pragma unroll
@@ -174,16 +199,23 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  TL_MARK(2);
 
   if (warp >= CONSUMER_WARPS) {
     // ================= producers: pack_a / pack_b equivalent =================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
     const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+#ifdef MYD_TIMELINE
+    if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
+#endif
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int m0, n0;
       unit_origin(u, m0, n0);
+#ifdef MYD_TIMELINE
+      if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[9] = gtimer();
+#endif
       // C block of the unit through CS ring slots (my_dgemm contract only:
       // the BLAS epilogue reads C at the end instead).  The copies are issued
       // while the consumers finish the previous unit, so the C load is off the
@@ -221,6 +253,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             const int col = pw * CW + lane;
             bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, rows * 8, &full_bar[slot]);
           }
+#ifdef MYD_TIMELINE
+          if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[10 + cs] = gtimer();
+#endif
         }
       }
       // Interior units with 16-byte aligned operands use the bulk-copy (TMA)
@@ -253,6 +288,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             const int nn = pw * RW + lane;
             bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
           }
+#ifdef MYD_TIMELINE
+          if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x && kt == 0) g_tl[7] = gtimer();
+#endif
           continue;
         }
         // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
@@ -319,44 +357,65 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     for (int j = 0; j < FN; ++j) fb[buf][j] = bs[j * 8 * BP];
   };
 
-  uint32_t g = 0;  // ring position (C blocks and slabs consumed so far)
+  // smem index of fragment pair (i, j) inside a C block staged at ring
+  // position gpos: column cl = wn*WN + 8j + r lives in slot gpos + cl / CPS at
+  // column cl % CPS (r < 8 and CPS a multiple of 8, so the slot offset is
+  // fixed per warp and j: one base register per slot, constant offsets).
+  auto c_index = [&](uint32_t gpos, int i, int j) -> int {
+    const int c8 = wn * WN + j * 8;
+    int so, ci;
+    if constexpr (CPS >= WN) {
+      so = (wn * WN) / CPS;
+      ci = (wn * WN) % CPS + j * 8 + r;
+    } else {
+      so = c8 / CPS;
+      ci = c8 % CPS + r;
+    }
+    return (int)((gpos + so) % STAGES) * SLOT + ci * CP + wm * WM + i * 8 + 2 * q;
+  };
+  const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+  double acc[FM][FN][2];
+  // The accumulator starts at C (_mk's tile load): the unit's C block is
+  // staged in CS ring slots ahead of its slabs.  BLAS epilogue: starts at 0.
+  auto load_c_block = [&](uint32_t gpos) {
+#ifdef MYD_FAST_PROFILE
+    long long c_t0 = clock64();
+#endif
+    if (ep.blas) {
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      return;
+    }
+    for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(gpos + cs) % STAGES], ((gpos + cs) / STAGES) & 1);
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gpos, i, j)]);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      }
+    __syncwarp();
+    if (lane == 0)
+      for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(gpos + cs) % STAGES]);
+#ifdef MYD_FAST_PROFILE
+    if (lane == 0) PROF_ADD(6, clock64() - c_t0);
+#endif
+  };
+  uint32_t g = 0;       // ring position (C blocks and slabs consumed so far)
+  if ((int)blockIdx.x < units) load_c_block(0);
   for (int u = blockIdx.x; u < units; u += gridDim.x, g += KT) {
     int m0, n0;
     unit_origin(u, m0, n0);
-    double acc[FM][FN][2];
     // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
     // thread's pair is two consecutive rows of one column: 16 contiguous
     // bytes in column-major C):  acc[i][j][e] = C(row0 + 8i + e, col0 + 8j).
     const int row0 = m0 + wm * WM + 2 * q;
     const int col0 = n0 + wn * WN + r;
-#ifdef MYD_FAST_PROFILE
-    long long c_t0 = clock64();
-#endif
-    if (!ep.blas) {  // the accumulator starts at C (_mk's tile load), staged in CS ring slots
-      for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(g + cs) % STAGES], ((g + cs) / STAGES) & 1);
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) {
-          const int cl = wn * WN + j * 8 + r, rl = wm * WM + i * 8 + 2 * q;
-          const double2 v = *reinterpret_cast<const double2 *>(
-              &smem[((g + cl / CPS) % STAGES) * SLOT + (cl % CPS) * CP + rl]);
-          acc[i][j][0] = v.x;
-          acc[i][j][1] = v.y;
-        }
-      __syncwarp();
-      if (lane == 0)
-        for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(g + cs) % STAGES]);
-      g += CS;
-    } else {
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    }
-#ifdef MYD_FAST_PROFILE
-    if (lane == 0) PROF_ADD(6, clock64() - c_t0);
-#endif
+    if (!ep.blas) g += CS;  // this unit's C block (already in acc)
+    TL_MARK(3);
 #ifdef MYD_FAST_PROFILE
     long long loop_t0 = clock64();
 #endif
@@ -364,6 +423,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       PROF_T0();
       mbar_wait(&full_bar[g % STAGES], (g / STAGES) & 1);
       if (lane == 0) PROF_ADD(4, clock64() - _pt0);
+      TL_MARK(4);
     }
     load_frags(0, g % STAGES, 0);
     for (int kt = 0; kt < KT; ++kt) {
@@ -406,8 +466,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       PROF_ADD(7, 1);
     }
 #endif
+    TL_MARK(5);
     // ---- epilogue: valid region only (padding rows never touched) ----
-    const bool vec_store = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+    const bool has_next = u + (int)gridDim.x < units;
+    const bool vec_store = c_aligned;
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -428,7 +490,15 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           if (pair) cp[1] = v1;
         }
       }
+    if (has_next) load_c_block(g + KT);
+    TL_MARK(6);
+#ifdef MYD_TIMELINE
+    ++unit_ord;
+#endif
   }
+#ifdef MYD_TIMELINE
+  if (tid == 0) atomicMax(&g_tl[1], gtimer());
+#endif
 }
 
 namespace {
@@ -556,6 +626,15 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
 
 }  // namespace myd
 
+#ifdef MYD_TIMELINE
+extern "C" __attribute__((visibility("default"))) void my_dgemm_timeline(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, myd::g_tl, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {~0ull};
+    cudaMemcpyToSymbol(myd::g_tl, z, sizeof z);
+  }
+}
+#endif
 #ifdef MYD_FAST_PROFILE
 extern "C" __attribute__((visibility("default"))) void my_dgemm_fast_profile(unsigned long long *out, int reset) {
   cudaMemcpyFromSymbol(out, myd::g_fast_prof, sizeof(unsigned long long) * 8);

@@ -13,23 +13,15 @@
 //   * each panel's C goes down as soon as it is final.
 // Pageable callers (numpy arrays, the reference's own Matrix objects) go
 // through a pinned staging ring filled and drained by a small pool of host
-// threads, so the DMA engines always see pinned memory.  Copies are pitched
-// (width rows*8): padding rows are never read or written and nothing past
-// (n-1)*ld+m is touched (matrix.py:5-6,42-45,58-61).
+// threads, so the DMA engines always see pinned memory (host_io.cuh).
 #include <algorithm>
-#include <atomic>
-#include <condition_variable>
-#include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <functional>
 #include <mutex>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "../../include/my_dgemm.h"
 #include "common.cuh"
+#include "host_io.cuh"
 
 namespace myd {
 
@@ -41,105 +33,13 @@ int capi_cuda_fail(cudaError_t e, const char *where);
 
 namespace {
 
-// ---- a small fork-free host thread pool for pitched copies ----
-class CopyPool {
- public:
-  static CopyPool &get() {
-    static CopyPool pool;
-    return pool;
-  }
-  // Run fn(i) for i in [0, n) on the pool and the calling thread; blocks.
-  void parallel_for(int n, const std::function<void(int)> &fn) {
-    if (n <= 1 || workers_.empty()) {
-      for (int i = 0; i < n; ++i) fn(i);
-      return;
-    }
-    std::unique_lock<std::mutex> lk(mu_);
-    job_ = &fn;
-    total_ = n;
-    next_.store(0);
-    done_ = 0;
-    ++gen_;
-    cv_.notify_all();
-    lk.unlock();
-    work();
-    lk.lock();
-    done_cv_.wait(lk, [&] { return done_ == total_; });
-    job_ = nullptr;
-  }
-
- private:
-  CopyPool() {
-    int want = 8;
-    if (const char *s = getenv("MY_DGEMM_HOST_THREADS")) want = std::max(1, atoi(s));
-    const int hw = (int)std::thread::hardware_concurrency();
-    if (hw > 0) want = std::min(want, hw);
-    for (int t = 1; t < want; ++t) workers_.emplace_back([this] { loop(); });
-  }
-  ~CopyPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto &t : workers_) t.join();
-  }
-  void loop() {
-    uint64_t seen = 0;
-    for (;;) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
-      if (stop_) return;
-      seen = gen_;
-      lk.unlock();
-      work();
-    }
-  }
-  void work() {
-    const std::function<void(int)> *fn = job_;
-    int did = 0;
-    for (int i = next_.fetch_add(1); i < total_; i = next_.fetch_add(1)) {
-      (*fn)(i);
-      ++did;
-    }
-    if (did) {
-      std::lock_guard<std::mutex> lk(mu_);
-      done_ += did;
-      if (done_ == total_) done_cv_.notify_all();
-    }
-  }
-  std::vector<std::thread> workers_;
-  std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(int)> *job_ = nullptr;
-  std::atomic<int> next_{0};
-  int total_ = 0, done_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
-};
-
-// pitched host copy of `cols` columns of `rows` doubles, split over the pool
-void host_copy_2d(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols) {
-  const int64_t bytes = rows * 8;
-  const int64_t per = std::max<int64_t>(1, (4 << 20) / std::max<int64_t>(bytes, 1));  // ~4 MB per task
-  const int tasks = (int)((cols + per - 1) / per);
-  CopyPool::get().parallel_for(tasks, [&](int t) {
-    const int64_t c0 = t * per, c1 = std::min<int64_t>(cols, c0 + per);
-    for (int64_t c = c0; c < c1; ++c) memcpy(dst + c * dpitch, src + c * spitch, (size_t)bytes);
-  });
-}
-
 struct Workspace {
   int device = -1;
   double *dA = nullptr, *dB = nullptr, *dC = nullptr;
   size_t capA = 0, capB = 0, capC = 0;
   cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_done, ev_out;
-  // pinned staging ring for pageable callers
-  static constexpr int NSTAGE = 6;
-  static constexpr size_t STAGE_BYTES = 32u << 20;
-  double *stage[NSTAGE] = {};
-  cudaEvent_t ev_stage[NSTAGE] = {};
+  hostio::StageRing stage;  // pinned staging ring for pageable callers
 };
 
 std::mutex g_ws_mutex;
@@ -174,119 +74,6 @@ cudaError_t ensure_streams(Workspace &w, size_t n_events) {
   return cudaSuccess;
 }
 
-cudaError_t ensure_stage(Workspace &w) {
-  cudaError_t e;
-  for (int i = 0; i < Workspace::NSTAGE; ++i) {
-    if (w.stage[i]) continue;
-    if ((e = cudaMallocHost((void **)&w.stage[i], Workspace::STAGE_BYTES)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&w.ev_stage[i], cudaEventDisableTiming)) != cudaSuccess) return e;
-  }
-  return cudaSuccess;
-}
-
-bool is_pinned(const void *p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
-// Moves pitched column blocks between host and device on the workspace
-// streams: straight DMA for pinned host memory, through the staging ring for
-// pageable memory (host threads fill/drain the ring; the issuing thread
-// blocks only on the copy work it must do itself).
-class Mover {
- public:
-  Mover(Workspace &w, bool staged) : w_(w), staged_(staged) {}
-
-  cudaError_t up(double *d, int64_t dpitch, const double *h, int64_t hpitch, int64_t rows, int64_t cols) {
-    if (!staged_ || rows * 8 > (int64_t)Workspace::STAGE_BYTES)  // a column larger than a stage: direct
-      return cudaMemcpy2DAsync(d, dpitch * 8, h, (size_t)hpitch * 8, (size_t)rows * 8, cols,
-                               cudaMemcpyHostToDevice, w_.s_h2d);
-    const int64_t per = std::max<int64_t>(1, (int64_t)(Workspace::STAGE_BYTES / 8) / rows);
-    for (int64_t c0 = 0; c0 < cols; c0 += per) {
-      const int64_t nc = std::min(per, cols - c0);
-      const int s = next();
-      cudaError_t e = cudaEventSynchronize(w_.ev_stage[s]);  // buffer free (its last DMA done)
-      if (e != cudaSuccess) return e;
-      host_copy_2d(w_.stage[s], rows, h + c0 * hpitch, hpitch, rows, nc);
-      e = cudaMemcpy2DAsync(d + c0 * dpitch, dpitch * 8, w_.stage[s], (size_t)rows * 8, (size_t)rows * 8, nc,
-                            cudaMemcpyHostToDevice, w_.s_h2d);
-      if (e != cudaSuccess) return e;
-      if ((e = cudaEventRecord(w_.ev_stage[s], w_.s_h2d)) != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  }
-
-  // Queue a download; staged pieces are copied out to the user buffer as
-  // their DMA completes (at the latest in finish()).
-  cudaError_t down(double *h, int64_t hpitch, const double *d, int64_t dpitch, int64_t rows, int64_t cols) {
-    if (!staged_ || rows * 8 > (int64_t)Workspace::STAGE_BYTES)
-      return cudaMemcpy2DAsync(h, (size_t)hpitch * 8, d, dpitch * 8, (size_t)rows * 8, cols,
-                               cudaMemcpyDeviceToHost, w_.s_d2h);
-    const int64_t per = std::max<int64_t>(1, (int64_t)(Workspace::STAGE_BYTES / 8) / rows);
-    for (int64_t c0 = 0; c0 < cols; c0 += per) {
-      const int64_t nc = std::min(per, cols - c0);
-      const int s = next();
-      cudaError_t e = drain_until_free(s);
-      if (e != cudaSuccess) return e;
-      e = cudaMemcpy2DAsync(w_.stage[s], (size_t)rows * 8, d + c0 * dpitch, dpitch * 8, (size_t)rows * 8, nc,
-                            cudaMemcpyDeviceToHost, w_.s_d2h);
-      if (e != cudaSuccess) return e;
-      if ((e = cudaEventRecord(w_.ev_stage[s], w_.s_d2h)) != cudaSuccess) return e;
-      pending_.push_back({s, h + c0 * hpitch, hpitch, rows, nc});
-    }
-    return cudaSuccess;
-  }
-
-  cudaError_t finish() {
-    while (!pending_.empty()) {
-      cudaError_t e = pop();
-      if (e != cudaSuccess) return e;
-    }
-    return cudaSuccess;
-  }
-
- private:
-  struct Out {
-    int s;
-    double *h;
-    int64_t hpitch, rows, cols;
-  };
-  int next() {
-    const int s = slot_;
-    slot_ = (slot_ + 1) % Workspace::NSTAGE;
-    return s;
-  }
-  cudaError_t pop() {
-    Out o = pending_.front();
-    pending_.pop_front();
-    cudaError_t e = cudaEventSynchronize(w_.ev_stage[o.s]);
-    if (e != cudaSuccess) return e;
-    host_copy_2d(o.h, o.hpitch, w_.stage[o.s], o.rows, o.rows, o.cols);
-    return cudaSuccess;
-  }
-  // Before reusing stage s for a download, copy out (in queue order) every
-  // pending piece up to the one that occupies s.
-  cudaError_t drain_until_free(int s) {
-    auto uses = [&] {
-      for (const Out &o : pending_)
-        if (o.s == s) return true;
-      return false;
-    };
-    while (uses()) {
-      cudaError_t e = pop();
-      if (e != cudaSuccess) return e;
-    }
-    return cudaEventSynchronize(w_.ev_stage[s]);
-  }
-  Workspace &w_;
-  bool staged_;
-  int slot_ = 0;
-  std::deque<Out> pending_;
-};
 
 }  // namespace
 
@@ -320,9 +107,9 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   if ((e = grow(&w.dA, &w.capA, (size_t)dlda * k * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(A)");
   if ((e = grow(&w.dB, &w.capB, (size_t)dldb * n * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(B)");
   if ((e = grow(&w.dC, &w.capC, (size_t)dldc * n * 8)) != cudaSuccess) return capi_cuda_fail(e, "cudaMalloc(C)");
-  const bool staged = !(is_pinned(A) && is_pinned(B) && is_pinned(C));
-  if (staged && (e = ensure_stage(w)) != cudaSuccess) return capi_cuda_fail(e, "pinned staging");
-  Mover mv(w, staged);
+  const bool staged = !(hostio::is_pinned(A) && hostio::is_pinned(B) && hostio::is_pinned(C));
+  if (staged && (e = w.stage.ensure(6)) != cudaSuccess) return capi_cuda_fail(e, "pinned staging");
+  hostio::Mover mv(staged ? &w.stage : nullptr, w.s_h2d, w.s_d2h);
   const Epilogue ep{};
 
   // Program order = issue order: every GEMM is queued right after the
@@ -379,13 +166,7 @@ void release_host_workspace() {
     if (w.dC) cudaFree(w.dC);
     w.dA = w.dB = w.dC = nullptr;
     w.capA = w.capB = w.capC = 0;
-    for (int i = 0; i < Workspace::NSTAGE; ++i) {
-      if (w.stage[i]) {
-        if (w.ev_stage[i]) cudaEventSynchronize(w.ev_stage[i]);
-        cudaFreeHost(w.stage[i]);
-      }
-      w.stage[i] = nullptr;
-    }
+    w.stage.release();
     cudaSetDevice(prev);
   }
 }

@@ -41,6 +41,7 @@ __all__ = [
     "b200_factory",
     "register",
     "my_dgemm",
+    "my_dgemm_multi",
     "dgemm_device",
     "fill_random_device",
     "operand_seed",
@@ -203,6 +204,26 @@ def my_dgemm(m: int, n: int, k: int, A: np.ndarray, lda: int, B: np.ndarray, ldb
     lib = _capi.load()
     _capi.check(lib.my_dgemm_ex(m, n, k, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc,
                                 _flags(exact), None))
+    return C
+
+
+def my_dgemm_multi(devices, m: int, n: int, k: int, A: np.ndarray, lda: int, B: np.ndarray, ldb: int,
+                   C: np.ndarray, ldc: int, exact: bool = False) -> np.ndarray:
+    """my_dgemm over several GPUs of this process (C ABI my_dgemm_multi[_ex]).
+    `devices`: a device count (GPUs 0..n-1) or an explicit list of device ids
+    (entries may repeat: each is its own column shard).  Host buffers;
+    synchronous; C is bitwise the single-device my_dgemm result."""
+    if m < 1 or n < 1 or k < 1:
+        raise ValueError(f"matrix dims must be positive, got m={m} n={n} k={k}")
+    Matrix(m, k, lda, A), Matrix(k, n, ldb, B), Matrix(m, n, ldc, C)
+    lib = _capi.load()
+    if isinstance(devices, int) and not exact:
+        _capi.check(lib.my_dgemm_multi(devices, m, n, k, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc))
+        return C
+    ids = list(range(devices)) if isinstance(devices, int) else [int(d) for d in devices]
+    arr = (ctypes.c_int * max(1, len(ids)))(*ids)
+    _capi.check(lib.my_dgemm_multi_ex(arr, len(ids), m, n, k, _ptr(A), lda, _ptr(B), ldb, _ptr(C), ldc,
+                                      _flags(exact)))
     return C
 
 

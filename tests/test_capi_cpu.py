@@ -160,3 +160,31 @@ def test_blas_quick_returns_touch_nothing(lib):
     assert np.all(c == 3.5)
     with pytest.raises(ValueError, match="EXACT"):
         engine.dgemm("N", "N", 2, 2, 2, 2.0, np.ones(4), 2, np.ones(4), 2, 1.0, np.ones(4), 2, exact=True)
+
+
+def test_multi_argument_checks_shifted_indices(lib):
+    """my_dgemm_multi(ngpu, ...) / my_dgemm_multi_ex(devices, ndev, ...):
+    status -i names the first bad argument, C untouched (no GPU here, so a
+    structurally valid call fails on device visibility)."""
+    import ctypes
+
+    c = np.full(16, 3.5)
+    a = np.ones(16)
+    p = a.ctypes.data
+    assert lib.my_dgemm_multi(0, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4) == -1
+    assert lib.my_dgemm_multi(1, 0, 4, 4, p, 4, p, 4, c.ctypes.data, 4) == -2
+    assert lib.my_dgemm_multi(1, 4, 4, 4, p, 3, p, 4, c.ctypes.data, 4) == -6
+    assert lib.my_dgemm_multi(1, 4, 4, 4, p, 4, p, 4, None, 4) == -9
+    devs = (ctypes.c_int * 2)(0, 0)
+    assert lib.my_dgemm_multi_ex(None, 2, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4, 0) == -1
+    assert lib.my_dgemm_multi_ex(devs, 0, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4, 0) == -2
+    assert lib.my_dgemm_multi_ex(devs, 2, 4, 4, 0, p, 4, p, 4, c.ctypes.data, 4, 0) == -5
+    assert lib.my_dgemm_multi_ex(devs, 2, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 3, 0) == -11
+    assert lib.my_dgemm_multi_ex(devs, 2, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4, 0x4) == -12
+    import torch
+
+    if not torch.cuda.is_available():
+        assert lib.my_dgemm_multi(1, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4) == -1
+        assert lib.my_dgemm_multi_ex(devs, 2, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4, 0) == -2
+        assert "not visible" in lib.my_dgemm_last_error().decode()
+    assert np.all(c == 3.5)

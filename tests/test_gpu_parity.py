@@ -425,6 +425,47 @@ def test_host_path_pageable_and_pinned_agree(torch_cuda, pinned):
     assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
 
 
+@pytest.mark.parametrize("shards,m,n,k,lds,pinned", [
+    (2, 1000, 1100, 700, None, False),
+    (3, 1500, 3000, 1000, (1507, 1003, 1501), False),
+    (4, 777, 1029, 4100, (781, 4105, 780), True),
+    (3, 100, 100, 300, None, False),       # n < one panel per shard: shards 1, 2 only upload A chunks
+    (2, 300, 1, 900, None, False),         # n == 1: the single-shard gemv, as my_dgemm
+    (3, 1, 700, 500, None, False),         # m == 1
+    (8, 640, 2048, 2048, None, True),
+])
+def test_multi_device_host_path_bitwise_equals_single(torch_cuda, shards, m, n, k, lds, pinned):
+    """my_dgemm_multi_ex over `shards` column shards (all on this GPU: the
+    device list repeats, each entry its own buffers, the A chunks still
+    travel shard to shard by peer copy) gives bitwise the single-device
+    my_dgemm result; padding rows untouched."""
+    lda, ldb, ldc = lds or (m, k, m)
+    a, b, c = oracle.make_padded_operands(SEED, m, n, k, lda, ldb, ldc, canary=-777.25)
+    want = engine.my_dgemm(m, n, k, a, lda, b, ldb, c.copy(), ldc)
+    if pinned:
+        ta, tb, tc = (torch_cuda.from_numpy(x).pin_memory() for x in (a, b, c))
+        got = engine.my_dgemm_multi([0] * shards, m, n, k, ta.numpy(), lda, tb.numpy(), ldb, tc.numpy(), ldc)
+    else:
+        got = engine.my_dgemm_multi([0] * shards, m, n, k, a, lda, b, ldb, c.copy(), ldc)
+    assert np.array_equal(oracle.valid_region(got, m, n, ldc), oracle.valid_region(want, m, n, ldc))
+    if ldc > m:
+        assert np.all(got.reshape(n, ldc)[:, m:] == -777.25)
+
+
+def test_multi_device_exact_mode_and_ngpu_entry(torch_cuda):
+    """Exact mode through the multi-device path is bitwise the naive oracle;
+    my_dgemm_multi(ngpu=1) is the single-device call."""
+    m, n, k = 97, 300, 83
+    a, b, c = oracle.make_operands(SEED, m, n, k)
+    want = oracle.naive(m, n, k, a, m, b, k, c.copy(), m)
+    got = engine.my_dgemm_multi([0, 0, 0], m, n, k, a, m, b, k, c.copy(), m, exact=True)
+    assert np.array_equal(got, want)
+    got1 = engine.my_dgemm_multi(1, m, n, k, a, m, b, k, c.copy(), m)
+    assert np.array_equal(got1, engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m))
+    with pytest.raises(ValueError, match="devices are visible"):
+        engine.my_dgemm_multi(torch_cuda.cuda.device_count() + 1, m, n, k, a, m, b, k, c.copy(), m)
+
+
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (1, 1, 777), (1, 5, 1), (5, 1, 1), (200, 300, 1), (2, 2, 4096)])
 def test_degenerate_shapes(torch_cuda, m, n, k):
     check_fast_vs_oracle(m, n, k, m + 1, k + 3, m + 2)
