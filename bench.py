@@ -11,8 +11,9 @@ C := A*B + C, m = k = 8192, fp64, column-major, tight leading dimensions,
 operands from the reference generator (seed 42, splitmix64-v1, generated on
 the device bit-exactly).  At N ranks the problem grows by columns (weak
 scaling): n = 8192*N, rank g owns columns [8192g, 8192(g+1)) of B and C, A
-lives on rank 0 and is broadcast in k-chunks over NCCL inside every step,
-overlapped with the per-rank GEMM (paper_1609_00076_b200/multi.py).  A step
+lives on rank 0 and is broadcast over NCCL inside every step before the
+per-rank GEMM (--overlap: in k-chunks under the GEMM; paper_1609_00076_b200/
+multi.py explains why that is not the default).  A step
 is one full C += A*B.  Inputs (3 x 512 MiB per rank) exceed the 126 MB L2,
 so no flush is needed between steps.
 
@@ -303,7 +304,7 @@ def run_b200_arm(args):
         e1.record(stream)
         launch_events.append((e0, e1, kc))
 
-    drv = ShardedDgemm(plan, rank, compute=timed_compute)
+    drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=args.overlap)
 
     def step():
         drv.step(A, m, B, k, C, m)
@@ -365,8 +366,9 @@ def run_b200_arm(args):
             "data": "synthetic (reference splitmix64-v1 generator, seed 42, generated on device bit-exactly)",
             "config": {"workload": args.workload, "m": m, "n": n_total, "k": k,
                        "n_per_gpu": nloc, "lda": m, "ldb": k, "ldc": m, "layout": "column-major",
-                       "parallelism": f"jc-shard x{world}" + (", NCCL broadcast of A in "
-                                                              f"{len(plan.chunks)} k-chunks" if world > 1 else ""),
+                       "parallelism": f"jc-shard x{world}" + (
+                           (f", NCCL broadcast of A in {len(plan.chunks)} k-chunks under the GEMM" if args.overlap
+                            else ", NCCL broadcast of A, then the GEMM") if world > 1 else ""),
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
@@ -459,6 +461,8 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2_8192")
     ap.add_argument("--k-chunk", type=int, default=2048)
+    ap.add_argument("--overlap", action="store_true",
+                    help="broadcast A in k-chunks under the GEMM instead of before it (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")

@@ -11,9 +11,11 @@ depends only on A and column j of B.  So:
   * rank g owns the contiguous column panel [j0_g, j1_g) of B and C
     (`split_columns`, the split_range rule, rounded to the 128-column CTA
     tile) -- B and C are never communicated;
-  * A (m x k) lives on `root` and is broadcast in k-chunks (`k_chunks`,
-    multiples of 16 = the kernel's K slab, so chunked accumulation is bitwise
-    the single call); chunk i+1 crosses NVLink while chunk i's GEMM runs;
+  * A (m x k) lives on `root` and is broadcast -- whole before the GEMM by
+    default, or in k-chunks (`k_chunks`, multiples of 16 = the kernel's K
+    slab, so chunked accumulation is bitwise the single call) with chunk i+1
+    crossing NVLink while chunk i's GEMM runs (overlap=True, see
+    ShardedDgemm);
   * each rank runs C_g += A[:, chunk] * B_g[chunk, :] in ascending chunk
     order (my_dgemm_shard), the reference's pc order, so C is bitwise
     identical for every world size.
@@ -101,8 +103,17 @@ class ShardedDgemm:
 
     def __init__(self, plan: ShardPlan, rank: int, group=None,
                  compute: Callable | None = None, broadcast: Callable | None = None,
-                 force_tiled: bool | None = None):
+                 force_tiled: bool | None = None, overlap: bool = False):
         self.plan, self.rank, self.group = plan, rank, group
+        # overlap=True: chunk c+1's broadcast runs under chunk c's GEMM.  Off by
+        # default: NCCL's broadcast kernels run on SMs, and the GEMM is a
+        # persistent kernel holding one CTA (224 KB of shared memory) on every
+        # SM -- a rank whose GEMM started first keeps its NCCL kernel off the
+        # SMs for a whole chunk while the peers' NCCL kernels spin on theirs,
+        # delaying their GEMM CTAs.  Without multi-GPU hardware to measure the
+        # overlap, the default moves all of A first (one broadcast, every rank
+        # waits for it) and then runs the GEMM alone; C is bitwise the same.
+        self.overlap = overlap
         # A rank whose panel is one column must not switch to the n==1 kernel
         # when the global problem is not n==1 (keeps C identical across world
         # sizes).
@@ -129,6 +140,13 @@ class ShardedDgemm:
         p = self.plan
         j0, j1 = p.local(self.rank)
         nloc = j1 - j0
+        if not self.overlap:
+            if p.world > 1 and broadcast_a:
+                lo, hi = a_span(lda, p.m, 0, p.k)
+                self._broadcast(A[lo:hi], p.root).wait()  # every rank, root included
+            if nloc > 0:
+                self._compute(p.m, nloc, p.k, A[:a_span(lda, p.m, 0, p.k)[1]], lda, B_local, ldb, C_local, ldc)
+            return C_local
         works = []
         if p.world > 1 and broadcast_a:
             for (p0, p1) in p.chunks:

@@ -70,7 +70,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, shape, lds, k_chunk, out_q):
+def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q):
     import oracle
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -91,7 +91,7 @@ def _worker(rank, world, port, shape, lds, k_chunk, out_q):
             calls.append(kc)
             oracle.naive(m_, nloc, kc, A_.numpy(), lda_, B_.numpy(), ldb_, C_.numpy(), ldc_)
 
-        drv = ShardedDgemm(plan, rank, compute=compute)
+        drv = ShardedDgemm(plan, rank, compute=compute, overlap=overlap)
         drv.step(A, lda, B_local, ldb, C_local, ldc)
         # valid region of A arrived; padding rows were never sent
         got_a = oracle.valid_region(A.numpy(), m, k, lda)
@@ -101,18 +101,19 @@ def _worker(rank, world, port, shape, lds, k_chunk, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,lds,k_chunk", [
-    ((37, 300, 71), (44, 76, 40), 32),
-    ((16, 129, 50), (16, 50, 16), 16),
+@pytest.mark.parametrize("shape,lds,k_chunk,overlap", [
+    ((37, 300, 71), (44, 76, 40), 32, True),
+    ((16, 129, 50), (16, 50, 16), 16, True),
+    ((37, 300, 71), (44, 76, 40), 32, False),
 ])
-def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk):
+def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk, overlap):
     import oracle
 
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, lds, k_chunk, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, lds, k_chunk, overlap, q)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
@@ -123,7 +124,7 @@ def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk):
     lda, ldb, ldc = lds
     a, b, c = oracle.make_padded_operands(42, m, n, k, lda, ldb, ldc, canary=-9.0)
     want = oracle.naive(m, n, k, a, lda, b, ldb, c.copy(), ldc)
-    nchunks = len(k_chunks(k, k_chunk))
+    nchunks = len(k_chunks(k, k_chunk)) if overlap else 1
     for rank, j0, j1, cl, calls, a_ok in sorted(results, key=lambda t: t[0]):
         assert a_ok, f"rank {rank} did not receive A"
         if j1 > j0:
