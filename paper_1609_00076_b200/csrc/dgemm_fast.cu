@@ -147,7 +147,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 template <int VEC, int BM, int BN, int BKT>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
-                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
                       int units, Epilogue ep) {
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
@@ -172,14 +172,36 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   // Work unit u (persistent CTA b takes u = b, b + gridDim.x, ...): full
   // 128x128 tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows
-  // per band, column-major inside a band), sub-block u % SPLIT of it.
+  // per band, column-major inside a band), sub-block u % SPLIT of it.  With
+  // edge_ns > 0 the ragged last tile column is kept out of the raster and
+  // its units follow the raster's: per tile row, the SPLIT_M x edge_ns
+  // sub-blocks that hold valid columns (launch_dgemm_fast's edge plan).
+  // Units wholly outside C are skipped.
+  const int raster_units = (tiles_m * tiles_n - tile0) * SPLIT;  // units of raster tiles in this launch
   auto unit_origin = [&](int u, int &m0, int &n0) {
+    if (edge_ns > 0 && u >= raster_units) {  // edge column: only its edge_ns valid strips per sub-row
+      const int e = u - raster_units, per = SPLIT_M * edge_ns, idx = e % per;
+      m0 = (e / per) * TILE_M + (idx / edge_ns) * BM;
+      n0 = tiles_n * TILE_N + (idx % edge_ns) * BN;
+      return;
+    }
     const int tile = tile0 + u / SPLIT, sub = u % SPLIT;
     const int band = GROUP_M * tiles_n;
     const int first_m = (tile / band) * GROUP_M;
     const int gm = min(tiles_m - first_m, GROUP_M);
     m0 = (first_m + (tile % band) % gm) * TILE_M + (sub / SPLIT_N) * BM;
     n0 = ((tile % band) / gm) * TILE_N + (sub % SPLIT_N) * BN;
+  };
+  // this CTA's next non-empty unit at or after u (u itself on this CTA's stride)
+  const bool ragged = (M % TILE_M) != 0 || (N % TILE_N) != 0;  // else no unit can be empty
+  auto next_unit = [&](int u) {
+    if (!ragged) return u;
+    for (; u < units; u += gridDim.x) {
+      int m0, n0;
+      unit_origin(u, m0, n0);
+      if (m0 < M && n0 < N) break;
+    }
+    return u;
   };
 
   const int tid = threadIdx.x;
@@ -210,7 +232,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
 #endif
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = next_unit(blockIdx.x); u < units; u = next_unit(u + gridDim.x)) {
       int m0, n0;
       unit_origin(u, m0, n0);
 #ifdef MYD_TIMELINE
@@ -405,8 +427,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #endif
   };
   uint32_t g = 0;       // ring position (C blocks and slabs consumed so far)
-  if ((int)blockIdx.x < units) load_c_block(0);
-  for (int u = blockIdx.x; u < units; u += gridDim.x, g += KT) {
+  int u_next = next_unit(blockIdx.x);
+  if (u_next < units) load_c_block(0);
+  for (int u = u_next; u < units; u = u_next, g += KT) {
+    u_next = next_unit(u + gridDim.x);
     int m0, n0;
     unit_origin(u, m0, n0);
     // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
@@ -468,7 +492,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #endif
     TL_MARK(5);
     // ---- epilogue: valid region only (padding rows never touched) ----
-    const bool has_next = u + (int)gridDim.x < units;
+    const bool has_next = u_next < units;
     const bool vec_store = c_aligned;
 #pragma unroll
     for (int i = 0; i < FM; ++i)
@@ -508,7 +532,7 @@ int sm_count();
 template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>()>
 cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                        const double *B,
-                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, cudaStream_t st) {
+                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns, cudaStream_t st) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
   // once per (device, instantiation); racing first calls just set it twice.
@@ -526,7 +550,7 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   // persistent: at most one CTA per SM, each walking units b, b+grid, ...
   const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
   dgemm_fast_kernel<VEC, BM, BN, BK>
-      <<<grid, THREADS, Ring<BM, BN, BK>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, (int)units,
+      <<<grid, THREADS, Ring<BM, BN, BK>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, (int)units,
                                                           ep);
   count_launch();
   return cudaGetLastError();
@@ -534,18 +558,18 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
 
 template <int VEC>
 cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
-                         const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                         const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
                          cudaStream_t st) {
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
         if (K >= 1024)  // long K: deeper slabs, fewer ring handshakes
-          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
       }
-      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
-    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, st);
+      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
+    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
+    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
+    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
   }
 }
 
@@ -569,8 +593,13 @@ int sm_count() {
 // into `split` units (128x64, 128x32 or 64x32; all 8 consumer warps busy)
 // when that shortens the last wave, whose cost is ceil(r*split/G)/split
 // tile-times.  Small problems (q = 0) therefore run entirely as small units.
-// force_split pins the plan (tests and the tuner): 0 = heuristic above,
-// 1 = full tiles only (no tail re-cut), 2 / 4 / 8 = every tile as units.
+// Ragged last tile column (N mod 128 in 1..64, e.g. cfg3a's n = 4099): the
+// plan may keep that column out of the full-tile raster and run it in the
+// tail launch as units, of which only those covering valid columns cost
+// anything (empty units are skipped), instead of paying full tiles for a few
+// columns.  force_split pins the plan (tests and the tuner): 0 = heuristic
+// above, 1 = full tiles only (no tail re-cut), 2 / 4 / 8 = every tile as
+// units.  Every plan computes bitwise the same C.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -581,6 +610,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   const bool vec2 =
       !force_vec1 && (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
   const long long G = sm_count();
+  int raster_n = tiles_n;  // tile columns in the grouped raster (the rest: edge column, appended)
+  int edge_ns = 0;         // edge plan: valid BN-wide strips of the edge column
   long long q = tiles / G, r = tiles % G;
   int split = 1;
   if (force_split > 1) {
@@ -589,39 +620,65 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     r = tiles;
   } else if (force_split == 1) {
     split = 1;
-  } else if (r > 0) {
+  } else {
     // Cost in full-tile times, smaller units discounted by their measured
     // efficiency (per-slab overhead grows as the unit shrinks):
-    //   full tiles + leftovers as s-units : q + ceil(r s / G) / (s eff_s)
+    //   full tiles + leftovers as s-units : q + ceil(u_s / G) / (s eff_s)
     //   every tile as 64x32 units         : ceil(8 T / G) / (8 eff_8)
+    // with u_s the non-empty s-units of the tail.
     auto eff = [](int s) { return s == 2 ? 0.97 : (s == 4 ? 0.95 : 0.92); };
-    double best = 1.0;  // leftovers as full tiles: one more round
-    for (int s : {2, 4, 8}) {
-      if (s == 8 && q > 0) continue;  // 64-high tail units only when nothing else runs
-      const double cost = (double)((r * s + G - 1) / G) / s / eff(s);
-      if (cost < best - 1e-9) {
-        best = cost;
-        split = s;
+    double best = r > 0 ? (double)q + 1.0 : (double)q;  // leftovers as full tiles: one more round
+    if (r > 0)
+      for (int s : {2, 4, 8}) {
+        if (s == 8 && q > 0) continue;  // 64-high tail units only when nothing else runs
+        const double cost = (double)q + (double)((r * s + G - 1) / G) / s / eff(s);
+        if (cost < best - 1e-9) {
+          best = cost;
+          split = s;
+        }
       }
-    }
     const double all8 = (double)((tiles * 8 + G - 1) / G) / 8 / eff(8);
-    if (q > 0 && all8 < (double)q + best - 1e-9) {  // e.g. 1792^3: 196 tiles on 148 SMs
+    if (q > 0 && all8 < best - 1e-9) {  // e.g. 1792^3: 196 tiles on 148 SMs
+      best = all8;
       split = 8;
       q = 0;
       r = tiles;
     }
+    const int rem_n = N % TILE_N;
+    if (rem_n >= 1 && rem_n <= 64 && tiles_n >= 2) {  // edge column out of the raster
+      const long long te = (long long)tiles_m * (tiles_n - 1);
+      const long long qe = te / G, re = te % G;
+      for (int s : {2, 4, 8}) {
+        if (s == 8 && qe > 0) continue;
+        const int ns = s == 2 ? 1 : (rem_n + 31) / 32;  // 128x64: 1 strip; 128x32 / 64x32: 32-wide strips
+        const long long nonempty = re * s + (long long)tiles_m * (s == 8 ? 2 : 1) * ns;
+        const double cost = (double)qe + (double)((nonempty + G - 1) / G) / s / eff(s);
+        if (cost < best - 1e-9) {
+          best = cost;
+          split = s;
+          raster_n = tiles_n - 1;
+          edge_ns = ns;
+          q = qe;
+          r = re;
+        }
+      }
+    }
   }
+  const long long raster_tiles = (long long)tiles_m * raster_n;
   const long long main_tiles = split == 1 ? tiles : q * G;
   cudaError_t e = cudaSuccess;
   if (main_tiles > 0)
-    e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream)
-             : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, stream);
+    e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
+                               stream)
+             : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
+                               stream);
   if (e != cudaSuccess || split == 1) return e;
-  const unsigned units = (unsigned)((tiles - main_tiles) * split);
-  return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
-                                stream)
-              : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, (int)main_tiles,
-                                stream);
+  const long long edge_units = edge_ns > 0 ? (long long)tiles_m * (split == 8 ? 2 : 1) * edge_ns : 0;
+  const unsigned units = (unsigned)((raster_tiles - main_tiles) * split + edge_units);
+  return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
+                                (int)main_tiles, edge_ns, stream)
+              : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
+                                (int)main_tiles, edge_ns, stream);
 }
 
 }  // namespace myd

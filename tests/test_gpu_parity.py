@@ -198,6 +198,8 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
     (1000, 1100, 300, 1000, 300, 1000),     # aligned: bulk-copy path
     (777, 1029, 201, 781, 205, 780),        # odd ld: 8-byte LDGSTS path
     (2304, 2304, 128, 2304, 128, 2304),     # plan picks tail strips (324 tiles)
+    (4093, 4099, 200, 4100, 202, 4096),     # ragged last tile column run as tail strips (edge plan)
+    (1500, 2050, 160, 1500, 160, 1503),     # edge plan, odd ldc, 2 valid columns in the edge tile
 ])
 def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     """Full tiles, 128x64 strips, 128x32 strips and 64x32 units give bitwise
