@@ -1,0 +1,80 @@
+"""The NCCL plumbing of the multi-GPU driver on the one GPU of the test box:
+a world-size-1 NCCL process group drives multi.ShardedDgemm for rank 0 of a
+2-way column split, with the A broadcast going through NCCL (rank 0 is the
+root, so no data moves, but the collective is issued on NCCL's stream and
+every chunk's GEMM waits on its work handle) -- in both schedules.  The
+panel must be bitwise the single-GPU call's columns; the timing all-reduce
+bench.py uses (MAX over ranks) is exercised too.  Ranks never wait on one
+another's kernels here (world size 1)."""
+
+import os
+import socket
+import subprocess
+import sys
+import textwrap
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = textwrap.dedent("""
+    import sys
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, {repo!r})
+    from paper_1609_00076_b200 import engine
+    from paper_1609_00076_b200.multi import ShardedDgemm, make_shard_plan
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    m, n, k = 1000, 1100, 900
+    st = torch.cuda.current_stream().cuda_stream
+    bufs = [torch.empty(x, dtype=torch.float64, device=dev) for x in (m * k, k * n, m * n)]
+    for t, (buf, r, c) in enumerate(zip(bufs, (m, k, m), (k, n, n))):
+        engine.fill_random_device(buf.data_ptr(), r, c, r, 11 + t, 0, st)
+    a, b, c0 = bufs
+    want = c0.clone()
+    engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, want.data_ptr(), m, st, force_tiled=True)
+    plan = make_shard_plan(m, n, k, 2, root=0, k_chunk=256)
+    j0, j1 = plan.local(0)
+
+    def bcast(t, src):
+        return dist.broadcast(t, src=src, async_op=True)
+
+    for overlap in (False, True):
+        got = c0.clone()
+        ShardedDgemm(plan, 0, broadcast=bcast, overlap=overlap).step(a, m, b[j0 * k:], k, got[j0 * m:], m)
+        torch.cuda.synchronize()
+        assert torch.equal(got[j0 * m:j1 * m], want[j0 * m:j1 * m]), overlap
+    t = torch.tensor([3.0, 1.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    assert float(t[0]) == 3.0
+    dist.destroy_process_group()
+    print("NCCL-OK", j0, j1, len(plan.chunks))
+""")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def test_nccl_world1_sharded_step_bitwise(tmp_path):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    script = tmp_path / "nccl_step.py"
+    script.write_text(SCRIPT.format(repo=REPO))
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1",
+               LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "NCCL-OK" in r.stdout
