@@ -589,17 +589,19 @@ int sm_count() {
 }  // namespace
 
 // Launch plan.  With G SMs (one persistent CTA each) and T full 128x128
-// tiles, T = q*G + r: q*G tiles run as full tiles; the r leftovers are cut
-// into `split` units (128x64, 128x32 or 64x32; all 8 consumer warps busy)
-// when that shortens the last wave, whose cost is ceil(r*split/G)/split
-// tile-times.  Small problems (q = 0) therefore run entirely as small units.
-// Ragged last tile column (N mod 128 in 1..64, e.g. cfg3a's n = 4099): the
-// plan may keep that column out of the full-tile raster and run it in the
-// tail launch as units, of which only those covering valid columns cost
-// anything (empty units are skipped), instead of paying full tiles for a few
-// columns.  force_split pins the plan (tests and the tuner): 0 = heuristic
-// above, 1 = full tiles only (no tail re-cut), 2 / 4 / 8 = every tile as
-// units.  Every plan computes bitwise the same C.
+// tiles, T = q*G + r, the candidates are: every tile as a full tile;
+// q*G full tiles plus the r leftovers cut into `split` units (128x64,
+// 128x32 or 64x32; all 8 consumer warps busy) in a second launch; every tile
+// as units.  Ragged last tile column (N mod 128 in 1..64, e.g. cfg3a's
+// n = 4099): the column may be kept out of the full-tile raster and run in
+// the tail launch as units, only those covering valid columns scheduled.
+// Each candidate is costed with the per-unit time measured on the B200
+// (tools/plan_probe.py, profiles/plan_probe_r01.log): a unit of s-th of a
+// tile at depth K takes ideal/e_s + b_s microseconds on one SM (ideal at
+// 128 flop/clk, 1.965 GHz), and a second launch costs ~15 us; the cheapest
+// wins.  force_split pins the plan (tests and the tuner): 0 = heuristic,
+// 1 = full tiles only, 2 / 4 / 8 = every tile as units.  Every plan
+// computes bitwise the same C.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -618,41 +620,48 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     split = force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2);  // every tile as units
     q = 0;
     r = tiles;
-  } else if (force_split == 1) {
-    split = 1;
-  } else {
-    // Cost in full-tile times, smaller units discounted by their measured
-    // efficiency (per-slab overhead grows as the unit shrinks):
-    //   full tiles + leftovers as s-units : q + ceil(u_s / G) / (s eff_s)
-    //   every tile as 64x32 units         : ceil(8 T / G) / (8 eff_8)
-    // with u_s the non-empty s-units of the tail.
-    auto eff = [](int s) { return s == 2 ? 0.97 : (s == 4 ? 0.95 : 0.92); };
-    double best = r > 0 ? (double)q + 1.0 : (double)q;  // leftovers as full tiles: one more round
-    if (r > 0)
-      for (int s : {2, 4, 8}) {
-        if (s == 8 && q > 0) continue;  // 64-high tail units only when nothing else runs
-        const double cost = (double)q + (double)((r * s + G - 1) / G) / s / eff(s);
-        if (cost < best - 1e-9) {
-          best = cost;
+  } else if (force_split == 0) {
+    auto unit_us = [&](int s) {  // one unit of 1/s tile, depth K, on one SM (fitted)
+      const double ideal = 2.0 * TILE_M * TILE_N / s * K / 251.5e3;
+      switch (s) {
+        case 1: return ideal / 0.990 + 2.8;
+        case 2: return ideal / 0.984 + 7.2;
+        case 4: return ideal / 0.983 + 4.4;
+        default: return ideal / 0.977 + 2.0;
+      }
+    };
+    auto rounds = [&](long long units) { return (double)((units + G - 1) / G); };
+    constexpr double SECOND_LAUNCH_US = 15.0;
+    double best = rounds(tiles) * unit_us(1);  // full tiles only
+    q = tiles;  // (split == 1: one launch of every tile)
+    for (int s : {2, 4, 8}) {
+      const double all = rounds(tiles * s) * unit_us(s);
+      if (all < best - 1e-9) {
+        best = all;
+        split = s;
+        q = 0;
+        r = tiles;
+      }
+      const long long q1 = tiles / G, r1 = tiles % G;
+      if (q1 > 0 && r1 > 0) {
+        const double tail = q1 * unit_us(1) + rounds(r1 * s) * unit_us(s) + SECOND_LAUNCH_US;
+        if (tail < best - 1e-9) {
+          best = tail;
           split = s;
+          q = q1;
+          r = r1;
         }
       }
-    const double all8 = (double)((tiles * 8 + G - 1) / G) / 8 / eff(8);
-    if (q > 0 && all8 < best - 1e-9) {  // e.g. 1792^3: 196 tiles on 148 SMs
-      best = all8;
-      split = 8;
-      q = 0;
-      r = tiles;
     }
     const int rem_n = N % TILE_N;
     if (rem_n >= 1 && rem_n <= 64 && tiles_n >= 2) {  // edge column out of the raster
       const long long te = (long long)tiles_m * (tiles_n - 1);
       const long long qe = te / G, re = te % G;
       for (int s : {2, 4, 8}) {
-        if (s == 8 && qe > 0) continue;
         const int ns = s == 2 ? 1 : (rem_n + 31) / 32;  // 128x64: 1 strip; 128x32 / 64x32: 32-wide strips
         const long long nonempty = re * s + (long long)tiles_m * (s == 8 ? 2 : 1) * ns;
-        const double cost = (double)qe + (double)((nonempty + G - 1) / G) / s / eff(s);
+        const double cost =
+            (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
         if (cost < best - 1e-9) {
           best = cost;
           split = s;
