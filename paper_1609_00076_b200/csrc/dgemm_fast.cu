@@ -28,6 +28,7 @@
 // the unit shape, the tile position, the K-slab depth or the launch plan, so
 // every plan and every k-chunking at multiples of 16 gives bitwise the same C.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <type_traits>
 
@@ -148,7 +149,7 @@ template <int VEC, int BM, int BN, int BKT>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
-                      int units, Epilogue ep) {
+                      int units, int after_main, Epilogue ep) {
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
   constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
@@ -222,6 +223,15 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   }
   __syncthreads();
   TL_MARK(2);
+  // Programmatic dependent launch (PDL): a call's first launch may start
+  // while the previous kernel in the stream drains, so it waits for that
+  // grid's completion (and memory flush) before touching global memory.  A
+  // call's tail launch works on tiles the main launch never touches and
+  // reads only A and B, so it starts as soon as SMs free up and waits at the
+  // very end instead (stream order of completion is kept).  Without the PDL
+  // launch attribute both are no-ops.
+  if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   if (warp >= CONSUMER_WARPS) {
     // ================= producers: pack_a / pack_b equivalent =================
@@ -360,6 +370,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       }
     }
     cp_async_wait<0>();
+    if (after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
     return;
   }
 
@@ -520,6 +531,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     ++unit_ord;
 #endif
   }
+  if (after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #ifdef MYD_TIMELINE
   if (tid == 0) atomicMax(&g_tl[1], gtimer());
 #endif
@@ -529,10 +541,20 @@ namespace {
 
 int sm_count();
 
+// PDL between consecutive launches (MY_DGEMM_NO_PDL=1 turns it off, for A/B timing).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("MY_DGEMM_NO_PDL");
+    return !(v && *v && *v != '0');
+  }();
+  return on;
+}
+
 template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>()>
 cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                        const double *B,
-                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns, cudaStream_t st) {
+                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
+                       int after_main, cudaStream_t st) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
   // once per (device, instantiation); racing first calls just set it twice.
@@ -549,27 +571,38 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   }
   // persistent: at most one CTA per SM, each walking units b, b+grid, ...
   const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
-  dgemm_fast_kernel<VEC, BM, BN, BK>
-      <<<grid, THREADS, Ring<BM, BN, BK>::BYTES, st>>>(M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, (int)units,
-                                                          ep);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = Ring<BM, BN, BK>::BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK>, M, N, K, A, lda, B, ldb, C, ldc,
+                                     tiles_m, tiles_n, tile0, edge_ns, (int)units, after_main, ep);
   count_launch();
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <int VEC>
 cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
+                         int after_main,
                          cudaStream_t st) {
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
         if (K >= 1024)  // long K: deeper slabs, fewer ring handshakes
-          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
+          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
       }
-      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
-    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
-    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
-    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, st);
+      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
+    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
+    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
+    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
   }
 }
 
@@ -614,12 +647,11 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   const long long G = sm_count();
   int raster_n = tiles_n;  // tile columns in the grouped raster (the rest: edge column, appended)
   int edge_ns = 0;         // edge plan: valid BN-wide strips of the edge column
-  long long q = tiles / G, r = tiles % G;
+  long long q = tiles / G;  // full-tile rounds of the main launch
   int split = 1;
   if (force_split > 1) {
     split = force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2);  // every tile as units
     q = 0;
-    r = tiles;
   } else if (force_split == 0) {
     auto unit_us = [&](int s) {  // one unit of 1/s tile, depth K, on one SM (fitted)
       const double ideal = 2.0 * TILE_M * TILE_N / s * K / 251.5e3;
@@ -640,7 +672,6 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         best = all;
         split = s;
         q = 0;
-        r = tiles;
       }
       const long long q1 = tiles / G, r1 = tiles % G;
       if (q1 > 0 && r1 > 0) {
@@ -649,7 +680,6 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
           best = tail;
           split = s;
           q = q1;
-          r = r1;
         }
       }
     }
@@ -668,7 +698,6 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
           raster_n = tiles_n - 1;
           edge_ns = ns;
           q = qe;
-          r = re;
         }
       }
     }
@@ -678,16 +707,16 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   cudaError_t e = cudaSuccess;
   if (main_tiles > 0)
     e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
-                               stream)
+                               0, stream)
              : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
-                               stream);
+                               0, stream);
   if (e != cudaSuccess || split == 1) return e;
   const long long edge_units = edge_ns > 0 ? (long long)tiles_m * (split == 8 ? 2 : 1) * edge_ns : 0;
   const unsigned units = (unsigned)((raster_tiles - main_tiles) * split + edge_units);
   return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
-                                (int)main_tiles, edge_ns, stream)
+                                (int)main_tiles, edge_ns, main_tiles > 0, stream)
               : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
-                                (int)main_tiles, edge_ns, stream);
+                                (int)main_tiles, edge_ns, main_tiles > 0, stream);
 }
 
 }  // namespace myd
