@@ -225,12 +225,13 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   TL_MARK(2);
   // Programmatic dependent launch (PDL): a call's first launch may start
   // while the previous kernel in the stream drains, so it waits for that
-  // grid's completion (and memory flush) before touching global memory.  A
+  // grid's completion (and memory flush) before touching global memory --
+  // the producers after working out their first unit, the consumers at once
+  // (their first global access comes after the producers' data anyway).  A
   // call's tail launch works on tiles the main launch never touches and
   // reads only A and B, so it starts as soon as SMs free up and waits at the
   // very end instead (stream order of completion is kept).  Without the PDL
   // launch attribute both are no-ops.
-  if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   if (warp >= CONSUMER_WARPS) {
@@ -242,9 +243,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
 #endif
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
-    for (int u = next_unit(blockIdx.x); u < units; u = next_unit(u + gridDim.x)) {
-      int m0, n0;
-      unit_origin(u, m0, n0);
+    int u = next_unit(blockIdx.x), m0 = 0, n0 = 0;
+    if (u < units) unit_origin(u, m0, n0);  // integer work, overlapping the previous grid's drain
+    if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    for (; u < units; u = next_unit(u + gridDim.x), unit_origin(u < units ? u : 0, m0, n0)) {
 #ifdef MYD_TIMELINE
       if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[9] = gtimer();
 #endif
@@ -375,6 +377,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   }
 
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+  if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
   // ================= consumers: loops 2/1 + micro-kernel =================
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int r = lane >> 2, q = lane & 3;
