@@ -48,10 +48,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define TL_MARK(i)                                                     \
   do {                                                                 \
-    if (blockIdx.x == 0 && tid == 0) {                                 \
+    if (blockIdx.x == 0 && tid == 0 && !after_main) {                  \
       const unsigned long long _t = gtimer();                          \
       if (unit_ord == 0) g_tl[i] = _t;                                 \
-      if (i >= 3 && unit_ord < 4) g_tl[16 + unit_ord * 4 + (i - 3)] = _t; \
+      if (i >= 3 && unit_ord >= 8 && unit_ord < 12)                    \
+        g_tl[16 + (unit_ord - 8) * 4 + (i - 3)] = _t;                  \
     }                                                                  \
   } while (0)
 #else

@@ -61,6 +61,6 @@ for m, n, k in shapes:
           flush=True)
     for o in range(4):
         cr, s0, le, ep = best[16 + 4 * o: 20 + 4 * o]
-        print(f"   unit {o}: C ready {cr:.2f}  slab0 {s0:.2f}  loop end {le:.2f}  epilogue {ep:.2f}  "
+        print(f"   unit {o + 8}: C ready {cr:.2f}  slab0 {s0:.2f}  loop end {le:.2f}  epilogue {ep:.2f}  "
               f"(loop {le - s0:.2f}, epi {ep - le:.2f})",
           flush=True)
