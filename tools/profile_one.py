@@ -8,11 +8,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1609_00076_b200 import engine
 
-args = [a for a in sys.argv[1:] if not a.startswith("--")]
-m, n, k = (int(x) for x in (args or [8192, 8192, 8192]))
+argv = sys.argv[1:]
 launches = 3
-if "--launches" in sys.argv:
-    launches = int(sys.argv[sys.argv.index("--launches") + 1])
+if "--launches" in argv:
+    i = argv.index("--launches")
+    launches = int(argv[i + 1])
+    del argv[i:i + 2]
+args = [a for a in argv if not a.startswith("--")]
+m, n, k = (int(x) for x in (args or [8192, 8192, 8192]))
 st = torch.cuda.current_stream().cuda_stream
 a = torch.empty(m * k, dtype=torch.float64, device="cuda")
 b = torch.empty(k * n, dtype=torch.float64, device="cuda")
