@@ -56,7 +56,7 @@ UNIT = "GFLOP/s"
 WORKLOADS = {
     # name: (m, n_per_rank, k)
     "cfg2_8192": (8192, 8192, 8192),
-    "cfg5": (32768, 32768, 32768),  # n is per rank here: use --strong for the 32768^3 split
+    "cfg5": (32768, 32768, 32768),  # n is per rank here; --strong splits the 32768^3 problem
     "cfg4": (16384, 16384, 256),
     "cfg3a": (4093, 4099, 2047),
 }
@@ -224,7 +224,8 @@ def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    m, n, k = WORKLOADS[args.workload]
+    m, n_rank, k = WORKLOADS[args.workload]
+    n = n_rank if args.strong else n_rank * max(world, args.gpus)  # the GPU arm's whole-job problem
     # each step a bounded slab so W+K steps finish within a few minutes
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     ref = CpuReference(m, n, k)
@@ -242,7 +243,7 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(flop_step / (value * 1e9) * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, seed 42)",
         "config": {"workload": args.workload, "m": m, "n": n, "k": k, "lda": m, "ldb": k, "ldc": m,
                    "layout": "column-major", "note": "each step times a column slab (cpu_baseline.sample)"},
@@ -273,7 +274,7 @@ def run_b200_arm(args):
     lib = _capi.load()
 
     m, n_rank, k = WORKLOADS[args.workload]
-    n_total = n_rank * world
+    n_total = n_rank if args.strong else n_rank * world  # strong: the workload's n split over the ranks
     plan = make_shard_plan(m, n_total, k, world, root=0, k_chunk=args.k_chunk)
     j0, j1 = plan.local(rank)
     nloc = j1 - j0
@@ -349,7 +350,7 @@ def run_b200_arm(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(args, m, nloc, k, seeds, j0, rank, world)
+        e2e = measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gf, info = cpu_reference_rate(m, n_total, k, target_s=args.cpu_seconds)
@@ -358,11 +359,11 @@ def run_b200_arm(args):
     if rank == 0:
         mean_kernel_s = sum(kern_ms) / len(kern_ms) * 1e-3
         achieved = (sum(kern_flop) / len(kern_flop)) / mean_kernel_s / 1e12
-        traffic = load_traffic()
+        traffic = load_traffic(args.workload)
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference splitmix64-v1 generator, seed 42, generated on device bit-exactly)",
             "config": {"workload": args.workload, "m": m, "n": n_total, "k": k,
                        "n_per_gpu": nloc, "lda": m, "ldb": k, "ldc": m, "layout": "column-major",
@@ -389,7 +390,7 @@ def run_b200_arm(args):
     return 0
 
 
-def measure_e2e(args, m, nloc, k, seeds, j0, rank, world):
+def measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total):
     """Same metric through the public host API: my_dgemm_ex on pinned host
     buffers (H2D of A, B_g, C_g and D2H of C_g every step), wall clock, max
     over ranks.  At N>1 every rank stages its own copy of A (a host-memory
@@ -435,22 +436,24 @@ def measure_e2e(args, m, nloc, k, seeds, j0, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t[0])
     lib.my_dgemm_release_workspace()
-    flop = 2.0 * m * nloc * k * world * steps
+    flop = 2.0 * m * n_total * k * steps
     return {"value": round(flop / dt / 1e9, 3), "unit": UNIT,
-            "h2d_bytes_per_step": 8 * (m * k + k * nloc + m * nloc) * world,
-            "d2h_bytes_per_step": 8 * m * nloc * world, "steps": steps,
+            "h2d_bytes_per_step": 8 * (m * k * world + (k + m) * n_total),
+            "d2h_bytes_per_step": 8 * m * n_total, "steps": steps,
             "api": "my_dgemm_ex(host pointers, pinned) -> panel-pipelined H2D/GEMM/D2H"}
 
 
-def load_traffic():
-    """dram bytes per launch of dgemm_fast_kernel from the committed ncu
-    --set full summary (profiles/), or None."""
+def load_traffic(workload):
+    """dram bytes per call of dgemm_fast_kernel from the committed ncu --set
+    full summary (profiles/traffic.json) when it was captured on this
+    workload, else None."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            t = json.load(f)
     except (OSError, ValueError):
         return None
+    return t.get("dram_bytes_per_launch") if str(t.get("workload", "")).startswith(workload + " ") else None
 
 
 def main():
@@ -461,6 +464,9 @@ def main():
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2_8192")
     ap.add_argument("--k-chunk", type=int, default=2048)
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the workload's n is the total, split over the ranks (e.g. "
+                         "--workload cfg5 --strong: SURVEY 8e's 32768^3 on 1/2/4/8 GPUs)")
     ap.add_argument("--overlap", action="store_true",
                     help="broadcast A in k-chunks under the GEMM instead of before it (N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
