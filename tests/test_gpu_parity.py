@@ -603,3 +603,33 @@ def test_cuda_graph_capture_and_replay(torch_cuda):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(graphed, eager)
+
+
+def test_more_than_2_31_elements_of_c(torch_cuda):
+    """C with 2.15e9 elements (> 2^31: every index is 64-bit): fast path vs the
+    exact kernel over the whole matrix within the headline bound, and the last
+    column's last element against a CPU evaluation of the same operands."""
+    m = n = 46341  # m * n = 2,147,488,281 > 2^31
+    k = 16
+    st = torch_cuda.cuda.current_stream().cuda_stream
+    free, _ = torch_cuda.cuda.mem_get_info()
+    if free < 3 * m * n * 8 + (1 << 30):
+        pytest.skip("needs ~52 GB of free device memory")
+    a = dev_matrix(torch_cuda, m, k, m, 101)
+    b = dev_matrix(torch_cuda, k, n, k, 102)
+    c0 = dev_matrix(torch_cuda, m, n, m, 103)
+    cf = c0.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, cf, m)
+    ce = c0
+    run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
+    bound = HEADLINE_C * k * EPS * (k + 1)  # |A|, |B|, |C| <= 1
+    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), m, ce.data_ptr(), m, bound)
+    assert i is None, (i, j, mx)
+    # last element, bitwise against the naive order evaluated on the host
+    row = a.view(k, m)[:, m - 1].cpu().numpy()
+    col = b.view(n, k)[n - 1].cpu().numpy()
+    del cf
+    want = float(dev_matrix(torch_cuda, m, n, m, 103)[(n - 1) * m + m - 1])
+    for p in range(k):
+        want = want + float(row[p]) * float(col[p])
+    assert float(ce[(n - 1) * m + m - 1]) == want
