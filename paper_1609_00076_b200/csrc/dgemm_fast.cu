@@ -231,9 +231,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (their first global access comes after the producers' data anyway).  A
   // call's tail launch works on tiles the main launch never touches and
   // reads only A and B, so it starts as soon as SMs free up and waits at the
-  // very end instead (stream order of completion is kept).  Without the PDL
-  // launch attribute both are no-ops.
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  // very end instead (stream order of completion is kept).  Dependents are
+  // released only once this grid has passed its own wait (the tail launch
+  // reads A and B, which the grid before the main launch may have written).
+  // Without the PDL launch attribute all of this is a no-op.
+  if (after_main) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   if (warp >= CONSUMER_WARPS) {
     // ================= producers: pack_a / pack_b equivalent =================
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
     int u = next_unit(blockIdx.x), m0 = 0, n0 = 0;
     if (u < units) unit_origin(u, m0, n0);  // integer work, overlapping the previous grid's drain
-    if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (!after_main) asm volatile("griddepcontrol.wait;\n" "griddepcontrol.launch_dependents;\n" ::: "memory");
     for (; u < units; u = next_unit(u + gridDim.x), unit_origin(u < units ? u : 0, m0, n0)) {
 #ifdef MYD_TIMELINE
       if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[9] = gtimer();
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   }
 
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
-  if (!after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  if (!after_main) asm volatile("griddepcontrol.wait;\n" "griddepcontrol.launch_dependents;\n" ::: "memory");
   // ================= consumers: loops 2/1 + micro-kernel =================
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int r = lane >> 2, q = lane & 3;

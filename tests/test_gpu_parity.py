@@ -633,3 +633,39 @@ def test_more_than_2_31_elements_of_c(torch_cuda):
     for p in range(k):
         want = want + float(row[p]) * float(col[p])
     assert float(ce[(n - 1) * m + m - 1]) == want
+
+
+@pytest.mark.parametrize("shape", [(2048, 2048, 2048), (1000, 1100, 700), (4093, 4099, 300)])
+def test_back_to_back_dependent_calls_stream_ordered(torch_cuda, shape):
+    """Consecutive calls on one stream with no host sync between them, each
+    reading the previous call's output (RAW) or overwriting its input (WAR):
+    programmatic dependent launch must keep stream semantics, including a
+    call's early-starting tail launch.  Compared with the same chain run with
+    a device sync after every call."""
+    m, n, k = shape
+    st = torch_cuda.cuda.current_stream().cuda_stream
+    base = [dev_matrix(torch_cuda, r, c, r, 300 + t) for t, (r, c) in
+            enumerate(((m, k), (k, n), (m, n), (m, n), (n, n)))]
+
+    def chain(sync):
+        a, b, c1, c2, b2 = (x.clone() for x in base)
+        calls = [
+            lambda: engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, c1.data_ptr(), m, st),
+            # RAW: c1 (just written) is the A operand
+            lambda: engine.dgemm_device(m, n, n, c1.data_ptr(), m, b2.data_ptr(), n, c2.data_ptr(), m, st),
+            # WAR: c1 (just read as A) is overwritten as C
+            lambda: engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, c1.data_ptr(), m, st),
+            # RAW again, chained through c2
+            lambda: engine.dgemm_device(m, n, n, c2.data_ptr(), m, b2.data_ptr(), n, c1.data_ptr(), m, st),
+        ]
+        for call in calls:
+            call()
+            if sync:
+                torch_cuda.cuda.synchronize()
+        torch_cuda.cuda.synchronize()
+        return c1, c2
+
+    want = chain(True)
+    for _ in range(3):
+        got = chain(False)
+        assert torch_cuda.equal(got[0], want[0]) and torch_cuda.equal(got[1], want[1])
