@@ -5,9 +5,12 @@
 //   loop 5/3 (jc, ic)  -> persistent CTAs (one per SM) walking 128x128 units of
 //                         C round-robin, rastered in bands of GROUP_M tile-rows
 //                         so co-resident CTAs share A and B panels in the
-//                         126 MB L2; the last partial wave (or a small
-//                         problem) is re-cut into 128x64 / 128x32 / 64x32
-//                         units so every SM gets work (launch_dgemm_fast);
+//                         126 MB L2; the last partial wave, a ragged last
+//                         tile column or a small problem is re-cut into
+//                         128x64 / 128x32 / 64x32 units so every SM gets work,
+//                         the plan chosen by a measured cost model
+//                         (launch_dgemm_fast); launches overlap their
+//                         neighbours by programmatic dependent launch;
 //   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs;
 //   pack_a / pack_b    -> producer warps stage each A and B slab (and, first,
 //                         the unit's C block) into a multi-stage shared-memory
@@ -37,9 +40,11 @@
 namespace myd {
 
 #ifdef MYD_TIMELINE
-// globaltimer (ns): [0] min CTA entry, [1] max CTA exit, CTA 0 / consumer warp 0:
-// [2] after barrier init, [3] C block ready, [4] first slab ready, [5] main loop
-// done, [6] epilogue stores issued (first unit)
+// globaltimer (ns), main launches only: [0] min CTA entry, [1] max CTA exit;
+// CTA 0 / consumer warp 0, first unit: [2] after barrier init, [3] unit start
+// (C in registers), [4] first slab ready, [5] main loop done, [6] stores issued
+// and next C block loaded; [16 + 4o + 0..3] the same marks 3..6 for units
+// 8..11; [7..12] producer warp 0 marks (tools/timeline_probe.py)
 __device__ unsigned long long g_tl[32];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
