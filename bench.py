@@ -305,7 +305,7 @@ def run_b200_arm(args):
         e1.record(stream)
         launch_events.append((e0, e1, kc))
 
-    drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=args.overlap)
+    drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=args.overlap, reserve_sms=args.reserve_sms)
 
     def step():
         drv.step(A, m, B, k, C, m)
@@ -469,6 +469,8 @@ def main():
                          "--workload cfg5 --strong: SURVEY 8e's 32768^3 on 1/2/4/8 GPUs)")
     ap.add_argument("--overlap", action="store_true",
                     help="broadcast A in k-chunks under the GEMM instead of before it (N>1)")
+    ap.add_argument("--reserve-sms", type=int, default=0,
+                    help="with --overlap: SMs kept free of the GEMM for NCCL's kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")

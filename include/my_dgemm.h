@@ -153,6 +153,16 @@ MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, in
 MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan, double *out_ms);
 MY_DGEMM_API void my_dgemm_tune_clear(void);
 
+/*
+ * Cap the persistent tiled kernel's grid at n CTAs (one per SM) for this
+ * process, leaving the other SMs to concurrent work -- e.g. the NCCL kernels
+ * of a broadcast overlapped with the GEMM (the reference's analogue is the
+ * thread count of gemm_goto_parallel, pkg/src/gemmforge/parallel.py:108-243).
+ * 0 = every SM (default).  Returns the previous cap, or -1 for n < 0.
+ * Results are bitwise independent of the cap.
+ */
+MY_DGEMM_API int my_dgemm_set_max_ctas(int n);
+
 /* Diagnostics. */
 MY_DGEMM_API const char *my_dgemm_last_error(void);
 MY_DGEMM_API int my_dgemm_last_status(void);

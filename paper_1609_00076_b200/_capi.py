@@ -44,6 +44,7 @@ SIGNATURES = {
                                    ctypes.POINTER(_I64), _P]),
     "my_dgemm_tune": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_D)]),
     "my_dgemm_tune_clear": (None, []),
+    "my_dgemm_set_max_ctas": (_I, [_I]),
     "my_dgemm_last_error": (ctypes.c_char_p, []),
     "my_dgemm_last_status": (_I, []),
     "my_dgemm_version": (ctypes.c_char_p, []),

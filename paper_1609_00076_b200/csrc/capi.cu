@@ -182,6 +182,7 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
               unsigned flags);
 void release_host_workspace();
 void release_multi_workspace();
+int set_max_ctas(int n);
 int multi_host_path(const int *devices, int G, int m, int n, int k, const double *A, int lda, const double *B,
                     int ldb, double *C, int ldc, unsigned flags);
 int capi_fail(int status, const std::string &msg) { return fail(status, msg); }
@@ -288,6 +289,11 @@ const char *my_dgemm_last_error(void) { return t_error.c_str(); }
 int my_dgemm_last_status(void) { return t_status; }
 const char *my_dgemm_version(void) { return "paper_1609_00076_b200 0.1.0 sm_100a dmma"; }
 uint64_t my_dgemm_kernel_launches(void) { return g_launches.load(); }
+
+int my_dgemm_set_max_ctas(int n) {
+  if (n < 0) return fail(-1, "max_ctas must be >= 0 (0 = every SM), got " + std::to_string(n));
+  return myd::set_max_ctas(n);
+}
 
 void my_dgemm_release_workspace(void) {
   myd::release_host_workspace();

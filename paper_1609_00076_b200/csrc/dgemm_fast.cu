@@ -617,6 +617,11 @@ cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, i
   }
 }
 
+std::atomic<int> g_max_ctas{0};  // my_dgemm_set_max_ctas: 0 = every SM
+
+// SMs the persistent grid may occupy: the device's count, or fewer when the
+// caller reserves SMs for concurrent work (e.g. NCCL kernels of an
+// overlapped broadcast).  Results do not depend on it.
 int sm_count() {
   static std::atomic<int> cached[64];
   int dev = 0;
@@ -627,10 +632,13 @@ int sm_count() {
     if (v <= 0) v = 148;
     cached[dev & 63].store(v, std::memory_order_relaxed);
   }
-  return v;
+  const int lim = g_max_ctas.load(std::memory_order_relaxed);
+  return (lim > 0 && lim < v) ? lim : v;
 }
 
 }  // namespace
+
+int set_max_ctas(int n) { return g_max_ctas.exchange(n); }
 
 // Launch plan.  With G SMs (one persistent CTA each) and T full 128x128
 // tiles, T = q*G + r, the candidates are: every tile as a full tile;

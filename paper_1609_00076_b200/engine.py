@@ -42,6 +42,7 @@ __all__ = [
     "register",
     "my_dgemm",
     "my_dgemm_multi",
+    "set_max_ctas",
     "dgemm_device",
     "fill_random_device",
     "operand_seed",
@@ -264,6 +265,15 @@ def max_abs_diff_device(m: int, n: int, x_ptr: int, ldx: int, y_ptr: int, ldy: i
         return mx.value, None, None
     j, i = divmod(first.value, m)
     return mx.value, i, j
+
+
+def set_max_ctas(n: int) -> int:
+    """Cap the tiled kernel at n SMs (0 = all); returns the previous cap.
+    Results are bitwise independent of the cap (my_dgemm_set_max_ctas)."""
+    prev = int(_capi.load().my_dgemm_set_max_ctas(int(n)))
+    if prev < 0:
+        raise ValueError(_capi.last_error())
+    return prev
 
 
 def kernel_launches() -> int:

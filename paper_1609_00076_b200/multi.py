@@ -103,8 +103,12 @@ class ShardedDgemm:
 
     def __init__(self, plan: ShardPlan, rank: int, group=None,
                  compute: Callable | None = None, broadcast: Callable | None = None,
-                 force_tiled: bool | None = None, overlap: bool = False):
+                 force_tiled: bool | None = None, overlap: bool = False, reserve_sms: int = 0):
         self.plan, self.rank, self.group = plan, rank, group
+        # overlap=True with reserve_sms > 0 caps the GEMM's persistent grid at
+        # (SM count - reserve_sms) CTAs during the step (my_dgemm_set_max_ctas)
+        # so the broadcast's NCCL kernels always find free SMs; C is unchanged.
+        self.reserve_sms = reserve_sms
         # overlap=True: chunk c+1's broadcast runs under chunk c's GEMM.  Off by
         # default: NCCL's broadcast kernels run on SMs, and the GEMM is a
         # persistent kernel holding one CTA (224 KB of shared memory) on every
@@ -147,6 +151,22 @@ class ShardedDgemm:
             if nloc > 0:
                 self._compute(p.m, nloc, p.k, A[:a_span(lda, p.m, 0, p.k)[1]], lda, B_local, ldb, C_local, ldc)
             return C_local
+        if self.reserve_sms > 0:
+            import torch
+
+            from .engine import set_max_ctas
+
+            sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            prev = set_max_ctas(max(1, sms - self.reserve_sms))
+            try:
+                return self._step_overlapped(A, lda, B_local, ldb, C_local, ldc, broadcast_a)
+            finally:
+                set_max_ctas(prev)
+        return self._step_overlapped(A, lda, B_local, ldb, C_local, ldc, broadcast_a)
+
+    def _step_overlapped(self, A, lda, B_local, ldb, C_local, ldc, broadcast_a):
+        p = self.plan
+        nloc = p.local(self.rank)[1] - p.local(self.rank)[0]
         works = []
         if p.world > 1 and broadcast_a:
             for (p0, p1) in p.chunks:

@@ -188,3 +188,13 @@ def test_multi_argument_checks_shifted_indices(lib):
         assert lib.my_dgemm_multi_ex(devs, 2, 4, 4, 4, p, 4, p, 4, c.ctypes.data, 4, 0) == -2
         assert "not visible" in lib.my_dgemm_last_error().decode()
     assert np.all(c == 3.5)
+
+
+def test_set_max_ctas_roundtrip(lib):
+    """my_dgemm_set_max_ctas: returns the previous cap, rejects n < 0."""
+    prev = lib.my_dgemm_set_max_ctas(100)
+    assert prev == 0
+    assert lib.my_dgemm_set_max_ctas(0) == 100
+    assert lib.my_dgemm_set_max_ctas(-3) == -1
+    assert "max_ctas" in lib.my_dgemm_last_error().decode()
+    assert lib.my_dgemm_set_max_ctas(0) == 0

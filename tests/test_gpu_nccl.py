@@ -44,11 +44,13 @@ SCRIPT = textwrap.dedent("""
     def bcast(t, src):
         return dist.broadcast(t, src=src, async_op=True)
 
-    for overlap in (False, True):
+    for overlap, reserve in ((False, 0), (True, 0), (True, 16)):
         got = c0.clone()
-        ShardedDgemm(plan, 0, broadcast=bcast, overlap=overlap).step(a, m, b[j0 * k:], k, got[j0 * m:], m)
+        ShardedDgemm(plan, 0, broadcast=bcast, overlap=overlap, reserve_sms=reserve).step(
+            a, m, b[j0 * k:], k, got[j0 * m:], m)
         torch.cuda.synchronize()
-        assert torch.equal(got[j0 * m:j1 * m], want[j0 * m:j1 * m]), overlap
+        assert torch.equal(got[j0 * m:j1 * m], want[j0 * m:j1 * m]), (overlap, reserve)
+    assert engine.set_max_ctas(0) == 0  # the step restored the cap
     t = torch.tensor([3.0, 1.0], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dist.barrier()

@@ -669,3 +669,22 @@ def test_back_to_back_dependent_calls_stream_ordered(torch_cuda, shape):
     for _ in range(3):
         got = chain(False)
         assert torch_cuda.equal(got[0], want[0]) and torch_cuda.equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("shape", [(4093, 4099, 300), (2048, 2048, 512), (700, 900, 1000)])
+def test_sm_cap_changes_speed_never_results(torch_cuda, shape):
+    """my_dgemm_set_max_ctas: the persistent grid on 100, 37 or 1 SMs gives
+    bitwise the all-SM result (different plans and unit assignment, same
+    per-element arithmetic)."""
+    m, n, k = shape
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    want = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, want, m)
+    try:
+        for cap in (100, 37, 1):
+            engine.set_max_ctas(cap)
+            got = c.clone()
+            run_dev(torch_cuda, m, n, k, a, m, b, k, got, m)
+            assert torch_cuda.equal(got, want), cap
+    finally:
+        engine.set_max_ctas(0)
