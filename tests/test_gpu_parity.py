@@ -688,3 +688,50 @@ def test_sm_cap_changes_speed_never_results(torch_cuda, shape):
             assert torch_cuda.equal(got, want), cap
     finally:
         engine.set_max_ctas(0)
+
+
+def test_concurrent_host_threads_disjoint_c(torch_cuda):
+    """Re-entrancy for disjoint C: host threads calling the
+    host-pointer path and the device path (each on its own stream) at the
+    same time get the results of sequential calls."""
+    import threading
+
+    shapes = [(700, 900, 500), (1024, 512, 768), (333, 1200, 257), (1500, 700, 900)]
+    ops = [oracle.make_operands(SEED + i, *s) for i, s in enumerate(shapes)]
+    want = [engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m) for (m, n, k), (a, b, c) in zip(shapes, ops)]
+    dev = []
+    for (m, n, k), (a, b, c) in zip(shapes, ops):
+        dev.append(tuple(torch_cuda.from_numpy(x).cuda() for x in (a, b, c)))
+    results, errors = {}, []
+
+    def host_worker(i):
+        try:
+            (m, n, k), (a, b, c) = shapes[i], ops[i]
+            for _ in range(3):
+                results[("h", i)] = engine.my_dgemm(m, n, k, a, m, b, k, c.copy(), m)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    def dev_worker(i):
+        try:
+            (m, n, k) = shapes[i]
+            a, b, c = dev[i]
+            s = torch_cuda.cuda.Stream()
+            with torch_cuda.cuda.stream(s):
+                cc = c.clone()
+                engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, cc.data_ptr(), m, s.cuda_stream)
+                s.synchronize()
+            results[("d", i)] = cc.cpu().numpy()
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    threads = [threading.Thread(target=host_worker, args=(i,)) for i in range(len(shapes))]
+    threads += [threading.Thread(target=dev_worker, args=(i,)) for i in range(len(shapes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for i in range(len(shapes)):
+        assert np.array_equal(results[("h", i)], want[i]), i
+        assert np.array_equal(results[("d", i)], want[i]), i
