@@ -1,5 +1,6 @@
 // dgemm_skinny.cu -- the HBM-bound shapes of the my_dgemm path (sm_100a):
 //   * n == 1 (cfg 3c): C(:,0) += A * B(:,0)          bytes 8(mk + k + 2m)
+//   * 2 <= n <= 16:    C(:,0:n) += A * B(:,0:n)      bytes 8(mk + kn + 2mn)
 //   * m == 1 (cfg 3b): C(0,:) += A(0,:) * B          bytes 8(k + kn + 2n)
 // Both stream one operand exactly once at full width, accumulate with FMA,
 // and reduce in a fixed order (no atomics, no workspace), so results are
@@ -74,6 +75,117 @@ __global__ void __launch_bounds__(32 * WARPS)
 }
 
 // ---------------------------------------------------------------------------
+// 2 <= n <= NC (a few right-hand sides: tall-skinny block updates).  The n == 1
+// kernel widened: a thread owns ROWS rows (32 apart, so every warp load is a
+// coalesced 256-byte column segment of A) and NC accumulators per row, so
+// each warp-uniform B(p, j) load (an L1 broadcast) feeds ROWS FMAs; A is
+// streamed once, 2n flop per 8 bytes.  Slice partials meet in shared memory
+// and are added in warp order per element.  HBM-bound up to n = 16
+// (4 flop/B); the tiled kernel would waste 1 - n/32 of every unit.
+// ---------------------------------------------------------------------------
+template <int NC, int ROWS, int WARPS, int KW>
+__global__ void __launch_bounds__(32 * WARPS)
+    gemm_nsmall_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                       int64_t ldb, double *__restrict__ C, int64_t ldc, Epilogue ep, int kchunk,
+                       double *__restrict__ work, unsigned *__restrict__ counters) {
+  constexpr int KS = WARPS * KW;               // k per staged sub-chunk (warp w: KW of them)
+  extern __shared__ double part[];             // [WARPS][ROWS * NC][32]; first 2 x KS x NC: B stages
+  double *bst = part;                          // B(p, 0..NC) rows of the current sub-chunk, 2 buffers
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row0 = blockIdx.x * 32 * ROWS + lane;  // rows row0 + 32 r
+  const int ks = blockIdx.y, nks = gridDim.y;     // this CTA's k-chunk
+  const int kb = ks * kchunk, ke = min(K, kb + kchunk);
+  double acc[ROWS][NC];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[r][j] = 0.0;
+  const double *a = A + row0;
+  bool ok[ROWS];
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) ok[r] = row0 + 32 * r < M;
+  // stage B(s .. s+KS, 0..N) into buffer `buf` (zeros past K / N)
+  auto stage = [&](int s, int buf) {
+    for (int t = threadIdx.x; t < KS * NC; t += 32 * WARPS) {
+      const int pp = t % KS, j = t / KS, p = s + pp;
+      bst[(buf * KS + pp) * NC + j] = (p < ke && j < N) ? __ldg(B + (int64_t)j * ldb + p) : 0.0;
+    }
+  };
+  int buf = 0;
+  stage(kb, 0);
+  __syncthreads();
+  for (int s = kb; s < ke; s += KS, buf ^= 1) {
+    if (s + KS < ke) stage(s + KS, buf ^ 1);  // next sub-chunk, behind this one's FMAs
+    const int pw = s + warp * KW;
+    double av[KW][ROWS];
+#pragma unroll
+    for (int u = 0; u < KW; ++u)
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+        av[u][r] = (ok[r] && pw + u < ke) ? __ldcs(a + (int64_t)(pw + u) * lda + 32 * r) : 0.0;
+#pragma unroll
+    for (int u = 0; u < KW; ++u) {
+      const double *bp = bst + (buf * KS + warp * KW + u) * NC;
+#pragma unroll
+      for (int j = 0; j < NC; j += 2) {
+        const double2 bv = *reinterpret_cast<const double2 *>(bp + j);
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          acc[r][j] = fma(av[u][r], bv.x, acc[r][j]);
+          acc[r][j + 1] = fma(av[u][r], bv.y, acc[r][j + 1]);
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` free, `buf ^ 1` complete
+  }
+  // partials of the WARPS warps per element (the B stages are no longer needed)
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) part[((warp * ROWS + r) * NC + j) * 32 + lane] = acc[r][j];
+  __syncthreads();
+  // element e = (r, j) of this CTA's ROWS x n block: warps take elements round-robin
+  if (nks == 1) {
+    for (int e = warp; e < ROWS * N; e += WARPS) {
+      const int r = e / N, j = e % N, row = row0 + 32 * r;
+      if (row >= M) continue;
+      double *cp = C + (int64_t)j * ldc + row;
+      double s = ep.blas ? 0.0 : *cp;
+      for (int w = 0; w < WARPS; ++w) s += part[((w * ROWS + r) * NC + j) * 32 + lane];
+      if (ep.blas) s = ep.beta == 0.0 ? ep.alpha * s : fma(ep.alpha, s, ep.beta * *cp);
+      *cp = s;
+    }
+    return;
+  }
+  // k split over nks CTAs: each writes its partial block to work[ks][j][row];
+  // the last CTA of the row block (counter) adds C + partial_0 + ... in order.
+  for (int e = warp; e < ROWS * N; e += WARPS) {
+    const int r = e / N, j = e % N, row = row0 + 32 * r;
+    if (row >= M) continue;
+    double s = 0.0;
+    for (int w = 0; w < WARPS; ++w) s += part[((w * ROWS + r) * NC + j) * 32 + lane];
+    work[((int64_t)ks * N + j) * M + row] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned last;
+  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1u) == (unsigned)(nks - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = warp; e < ROWS * N; e += WARPS) {
+    const int r = e / N, j = e % N, row = row0 + 32 * r;
+    if (row >= M) continue;
+    double *cp = C + (int64_t)j * ldc + row;
+    double s = ep.blas ? 0.0 : *cp;
+    for (int q = 0; q < nks; ++q) s += __ldcg(&work[((int64_t)q * N + j) * M + row]);
+    if (ep.blas) s = ep.beta == 0.0 ? ep.alpha * s : fma(ep.alpha, s, ep.beta * *cp);
+    *cp = s;
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0;  // ready for the next call's reuse
+}
+
+// ---------------------------------------------------------------------------
 // m == 1.  Teams of TEAM warps own columns (round-robin over all teams of the
 // grid); warp t of a team reduces k-quarter t of the column with lane-strided
 // coalesced loads, then the team combines its TEAM partials in order behind
@@ -128,20 +240,72 @@ __global__ void __launch_bounds__(32 * TEAM * M1_TEAMS, 1)
   }
 }
 
-namespace {
 int sm_count_skinny() {
   int dev = 0, v = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
   return v > 0 ? v : 148;
 }
-}  // namespace
 
 cudaError_t launch_gemv_n1(int M, int K, const double *A, int64_t lda, const double *b, double *C,
                            cudaStream_t stream, const Epilogue &ep) {
   gemv_n1_kernel<MYD_N1_WARPS, MYD_N1_UNROLL><<<(M + 31) / 32, 32 * MYD_N1_WARPS, 0, stream>>>(M, K, A, lda, b, C, ep);
   count_launch();
   return cudaGetLastError();
+}
+
+void keep_pool_memory();
+int sm_count_skinny();
+
+namespace {
+template <int NC, int ROWS, int WARPS, int KW>
+cudaError_t launch_nsmall_t(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                            double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  constexpr size_t part_bytes = (size_t)WARPS * ROWS * NC * 32 * 8, stage_bytes = (size_t)2 * WARPS * KW * NC * 8;
+  constexpr size_t smem = part_bytes > stage_bytes ? part_bytes : stage_bytes;
+  if constexpr (smem > 48 * 1024) {
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_nsmall_kernel<NC, ROWS, WARPS, KW>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_done.fetch_or(bit, std::memory_order_release);
+    }
+  }
+  // Enough CTAs to keep every SM streaming: split k (chunks of >= 512) when
+  // the row blocks alone do not cover 2 CTAs per SM.
+  const int row_blocks = (M + 32 * ROWS - 1) / (32 * ROWS);
+  const int want = (2 * sm_count_skinny() + row_blocks - 1) / row_blocks;
+  const int nks = std::max(1, std::min({want, (K + 511) / 512, 64}));
+  const int kchunk = (K + nks - 1) / nks;
+  double *work = nullptr;
+  unsigned *counters = nullptr;
+  if (nks > 1) {
+    keep_pool_memory();
+    cudaError_t e = cudaMallocAsync((void **)&work, (size_t)nks * N * M * 8 + (size_t)row_blocks * 4 + 16, stream);
+    if (e != cudaSuccess) return e;
+    counters = reinterpret_cast<unsigned *>(work + (size_t)nks * N * M);
+    if ((e = cudaMemsetAsync(counters, 0, (size_t)row_blocks * 4, stream)) != cudaSuccess) return e;
+  }
+  gemm_nsmall_kernel<NC, ROWS, WARPS, KW><<<dim3(row_blocks, nks), 32 * WARPS, smem, stream>>>(
+      M, N, K, A, lda, B, ldb, C, ldc, ep, kchunk, work, counters);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (work) cudaFreeAsync(work, stream);
+  return e;
+}
+}  // namespace
+
+// 2 <= N <= 16 columns (dispatch checks).
+cudaError_t launch_gemm_nsmall(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  if (N <= 2) return launch_nsmall_t<2, 4, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (N <= 4) return launch_nsmall_t<4, 4, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (N <= 8) return launch_nsmall_t<8, 2, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_nsmall_t<16, 2, 8, 4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
 }
 
 cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

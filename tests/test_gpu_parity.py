@@ -735,3 +735,34 @@ def test_concurrent_host_threads_disjoint_c(torch_cuda):
     for i in range(len(shapes)):
         assert np.array_equal(results[("h", i)], want[i]), i
         assert np.array_equal(results[("d", i)], want[i]), i
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (4096, 2, 3000, 4096, 3000, 4096),      # k split over CTAs, ordered fix-up
+    (5000, 7, 1000, 5003, 1001, 5002),      # odd lds, ragged row block
+    (8192, 16, 2048, 8192, 2048, 8195),
+    (4100, 3, 100, 4100, 100, 4100),        # single k chunk
+])
+def test_few_columns_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
+    """2 <= n <= 16 with a tall A runs on the bandwidth kernel: within the
+    headline bound of the exact kernel, deterministic, padding untouched;
+    the BLAS epilogue (beta = 0 on a NaN-filled C) through the same kernel."""
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
+    cf, ce = c.clone(), c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    bound = HEADLINE_C * k * EPS * (k + 1)
+    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
+    assert i is None, (i, j, mx)
+    again = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc)
+    assert torch_cuda.equal(again, cf)
+    host = cf.cpu().numpy().reshape(n, ldc)
+    if ldc > m:
+        assert np.all(host[:, m:] == -777.25)
+    cn = torch_cuda.full_like(c, float("nan"))
+    engine.dgemm("N", "N", m, n, k, 1.0, a.view(-1), lda, b.view(-1), ldb, 0.0, cn, ldc)
+    torch_cuda.cuda.synchronize()
+    prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
+    got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
+    assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
