@@ -2,9 +2,10 @@
 //   * n == 1 (cfg 3c): C(:,0) += A * B(:,0)          bytes 8(mk + k + 2m)
 //   * 2 <= n <= 16:    C(:,0:n) += A * B(:,0:n)      bytes 8(mk + kn + 2mn)
 //   * m == 1 (cfg 3b): C(0,:) += A(0,:) * B          bytes 8(k + kn + 2n)
-// Both stream one operand exactly once at full width, accumulate with FMA,
-// and reduce in a fixed order (no atomics, no workspace), so results are
-// deterministic and independent of the grid.  The reference computes these
+// Each streams the big operand exactly once at full width, accumulates with
+// FMA and reduces partial sums in a fixed order (the few-column kernel's k
+// split adds its per-CTA partials in chunk order in the last CTA of a row
+// block), so results are deterministic run to run.  The reference computes these
 // shapes with the same five-loop code as every other shape
 // (goto.py:187-239); on the GPU they are bandwidth problems, not DMMA ones.
 #include <algorithm>
