@@ -31,6 +31,8 @@ cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const dou
                            int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_gemm_nsmall(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep);
+cudaError_t launch_gemm_msmall(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
                                cudaStream_t stream);
 cudaError_t launch_copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
@@ -71,6 +73,9 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     // a few columns of a tall A: the bandwidth kernel (measured faster than
     // the tiled kernel from m = 4096, tools/nsmall_probe.py)
     if (n <= 16 && m >= 4096) return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
+    // a few rows of a wide B: its mirror (tools/msmall_probe.py)
+    if (m <= 16 && (n >= 8192 || (m <= 8 && n >= 4096)))
+      return launch_gemm_msmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
   }
   int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
               : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4

@@ -1,6 +1,7 @@
 // dgemm_skinny.cu -- the HBM-bound shapes of the my_dgemm path (sm_100a):
 //   * n == 1 (cfg 3c): C(:,0) += A * B(:,0)          bytes 8(mk + k + 2m)
 //   * 2 <= n <= 16:    C(:,0:n) += A * B(:,0:n)      bytes 8(mk + kn + 2mn)
+//   * 2 <= m <= 16:    C(0:m,:) += A(0:m,:) * B      bytes 8(mk + kn + 2mn)
 //   * m == 1 (cfg 3b): C(0,:) += A(0,:) * B          bytes 8(k + kn + 2n)
 // Each streams the big operand exactly once at full width, accumulates with
 // FMA and reduces partial sums in a fixed order (the few-column kernel's k
@@ -187,6 +188,103 @@ __global__ void __launch_bounds__(32 * WARPS)
 }
 
 // ---------------------------------------------------------------------------
+// 2 <= m <= MC (a few rows: wide-short updates).  B is the big operand, k
+// contiguous per column: each warp owns one column at a time and streams it
+// with coalesced lane-strided loads (two k per lane per step); the m rows of
+// A for the current k-chunk sit in shared memory ([i][p], conflict-free), so
+// every B value feeds m FMAs.  Lane partials are reduced by shuffles in a
+// fixed tree order, per row.  A chunk is re-read from L2 by every CTA
+// (m * K * 8 bytes, small); B is read once.
+// ---------------------------------------------------------------------------
+template <int MC, int MAXC, int WARPS, int KC>
+__global__ void __launch_bounds__(32 * WARPS)
+    gemm_msmall_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
+                       int64_t ldb, double *__restrict__ C, int64_t ldc, Epilogue ep) {
+  extern __shared__ double as[];  // [MC][KC]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this CTA's columns: j0 + warp, j0 + warp + WARPS, ... (COLS per warp)
+  const int64_t cols_per_cta = (int64_t)WARPS * ((N + (int64_t)gridDim.x * WARPS - 1) / ((int64_t)gridDim.x * WARPS));
+  const int64_t j_begin = (int64_t)blockIdx.x * cols_per_cta, j_end = min((int64_t)N, j_begin + cols_per_cta);
+  const int ncols = (int)((cols_per_cta + WARPS - 1) / WARPS);
+  for (int c0 = 0; c0 < ncols; c0 += MAXC) {
+    double acc[MAXC][MC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+      for (int i = 0; i < MC; ++i) acc[c][i] = 0.0;
+    for (int kb = 0; kb < K; kb += KC) {
+      const int kc = min(KC, K - kb);
+      __syncthreads();  // previous chunk consumed
+      for (int t = threadIdx.x; t < MC * KC; t += 32 * WARPS) {
+        const int i = t / KC, p = t % KC;
+        as[t] = (i < M && p < kc) ? __ldg(A + (int64_t)(kb + p) * lda + i) : 0.0;
+      }
+      __syncthreads();
+      // every A value read from shared memory feeds MAXC columns; UNROLL k
+      // steps of B loads are issued before their FMAs
+      const double *bc[MAXC];
+      bool live[MAXC];
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c) {
+        const int64_t j = j_begin + warp + (int64_t)(c0 + c) * WARPS;
+        live[c] = j < j_end;
+        bc[c] = B + (live[c] ? j : 0) * ldb + kb;
+      }
+      constexpr int UNROLL = 4;
+      int p = lane;
+      for (; p + 32 * (UNROLL - 1) < kc; p += 32 * UNROLL) {
+        double bv[UNROLL][MAXC];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) bv[u][c] = live[c] ? __ldcs(bc[c] + p + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+          for (int i = 0; i < MC; ++i) {
+            const double av = as[i * KC + p + 32 * u];
+#pragma unroll
+            for (int c = 0; c < MAXC; ++c) acc[c][i] = fma(av, bv[u][c], acc[c][i]);
+          }
+      }
+      for (; p < kc; p += 32) {
+        double bv[MAXC];
+#pragma unroll
+        for (int c = 0; c < MAXC; ++c) bv[c] = live[c] ? __ldcs(bc[c] + p) : 0.0;
+#pragma unroll
+        for (int i = 0; i < MC; ++i) {
+          const double av = as[i * KC + p];
+#pragma unroll
+          for (int c = 0; c < MAXC; ++c) acc[c][i] = fma(av, bv[c], acc[c][i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      const int64_t j = j_begin + warp + (int64_t)(c0 + c) * WARPS;
+#pragma unroll
+      for (int i = 0; i < MC; ++i) {
+        double v = acc[c][i];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        acc[c][i] = v;
+      }
+      if (j < j_end && lane < M && lane < MC) {
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < MC; ++i)
+          if (i == lane) v = acc[c][i];
+        double *cp = C + j * ldc + lane;
+        double s = ep.blas ? 0.0 : *cp;
+        s += v;
+        if (ep.blas) s = ep.beta == 0.0 ? ep.alpha * v : fma(ep.alpha, v, ep.beta * *cp);
+        *cp = s;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // m == 1.  Teams of TEAM warps own columns (round-robin over all teams of the
 // grid); warp t of a team reduces k-quarter t of the column with lane-strided
 // coalesced loads, then the team combines its TEAM partials in order behind
@@ -307,6 +405,56 @@ cudaError_t launch_gemm_nsmall(int M, int N, int K, const double *A, int64_t lda
   if (N <= 4) return launch_nsmall_t<4, 4, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
   if (N <= 8) return launch_nsmall_t<8, 2, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
   return launch_nsmall_t<16, 2, 8, 4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+}
+
+namespace {
+template <int MC, int MAXC, int WARPS, int KC>
+cudaError_t launch_msmall_t(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                            double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  constexpr size_t smem = (size_t)MC * KC * 8;
+  if constexpr (smem > 48 * 1024) {
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_msmall_kernel<MC, MAXC, WARPS, KC>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_done.fetch_or(bit, std::memory_order_release);
+    }
+  }
+  // each warp holds MAXC columns at a time; at most ~4 CTAs per SM
+  const int64_t want = std::min<int64_t>((N + (int64_t)WARPS * MAXC - 1) / ((int64_t)WARPS * MAXC),
+                                         4LL * sm_count_skinny());
+  gemm_msmall_kernel<MC, MAXC, WARPS, KC>
+      <<<(unsigned)want, 32 * WARPS, smem, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, ep);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// columns per warp held in registers: enough columns per warp for ~2 CTAs
+// per SM, at most 32 / MC (register budget)
+template <int MC>
+cudaError_t launch_msmall_cols(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  constexpr int WARPS = 8, KC = MC >= 16 ? 512 : 1024;
+  const int64_t per_warp = N / ((int64_t)WARPS * 2 * sm_count_skinny());
+  if constexpr (32 / MC >= 8)
+    if (per_warp >= 8) return launch_msmall_t<MC, 8, WARPS, KC>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if constexpr (32 / MC >= 4)
+    if (per_warp >= 4) return launch_msmall_t<MC, 4, WARPS, KC>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (per_warp >= 2) return launch_msmall_t<MC, 2, WARPS, KC>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_msmall_t<MC, 1, WARPS, KC>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+}
+}  // namespace
+
+// 2 <= M <= 16 rows (dispatch checks).
+cudaError_t launch_gemm_msmall(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  if (M <= 4) return launch_msmall_cols<4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (M <= 8) return launch_msmall_cols<8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_msmall_cols<16>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
 }
 
 cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

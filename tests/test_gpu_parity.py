@@ -766,3 +766,33 @@ def test_few_columns_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
     got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
     assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (4, 8192, 3000, 4, 3000, 4),
+    (7, 5000, 1000, 9, 1003, 8),            # odd / padded lds, ragged column groups
+    (16, 8192, 700, 16, 701, 19),
+    (2, 4100, 100, 2, 100, 2),
+])
+def test_few_rows_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
+    """2 <= m <= 16 with a wide B runs on the few-row kernel: within the
+    headline bound of the exact kernel, deterministic, padding untouched, and
+    the BLAS epilogue (beta = 0 on a NaN-filled C) through it."""
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
+    cf, ce = c.clone(), c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    bound = HEADLINE_C * k * EPS * (k + 1)
+    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
+    assert i is None, (i, j, mx)
+    again = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc)
+    assert torch_cuda.equal(again, cf)
+    if ldc > m:
+        assert np.all(cf.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
+    cn = torch_cuda.full_like(c, float("nan"))
+    engine.dgemm("N", "N", m, n, k, 1.0, a.view(-1), lda, b.view(-1), ldb, 0.0, cn, ldc)
+    torch_cuda.cuda.synchronize()
+    prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
+    got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
+    assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
