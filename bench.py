@@ -301,7 +301,7 @@ def run_b200_arm(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         engine.dgemm_device(mm, nl, kc, A_.data_ptr(), lda, B_.data_ptr(), ldb, C_.data_ptr(), ldc,
-                            st, force_tiled=n_total > 1)
+                            st, force_tiled=drv.force_tiled)
         e1.record(stream)
         launch_events.append((e0, e1, kc))
 

@@ -163,6 +163,22 @@ MY_DGEMM_API void my_dgemm_tune_clear(void);
  */
 MY_DGEMM_API int my_dgemm_set_max_ctas(int n);
 
+/*
+ * The kernel family a call of this shape and these flags runs on: the tiled
+ * DMMA kernel, or one of the bandwidth kernels for a short dimension.  Tiled
+ * calls of one problem are bitwise invariant to column sharding, k-chunking
+ * (multiples of 16) and launch plan; sharded drivers therefore pass
+ * MY_DGEMM_FORCE_TILED to every shard exactly when the whole problem's path
+ * is MY_DGEMM_PATH_TILED.  Negative status for m or n < 1.
+ */
+#define MY_DGEMM_PATH_TILED 0
+#define MY_DGEMM_PATH_GEMV_N1 1  /* n == 1 */
+#define MY_DGEMM_PATH_GEMV_M1 2  /* m == 1 */
+#define MY_DGEMM_PATH_FEW_COLS 3 /* 2 <= n <= 16, m >= 4096 */
+#define MY_DGEMM_PATH_FEW_ROWS 4 /* 2 <= m <= 8 */
+#define MY_DGEMM_PATH_EXACT 5    /* MY_DGEMM_EXACT */
+MY_DGEMM_API int my_dgemm_path(int m, int n, unsigned flags);
+
 /* Diagnostics. */
 MY_DGEMM_API const char *my_dgemm_last_error(void);
 MY_DGEMM_API int my_dgemm_last_status(void);

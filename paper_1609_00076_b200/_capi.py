@@ -22,6 +22,7 @@ FORCE_VEC1 = 0x8
 FORCE_STRIPS2 = 0x10
 FORCE_STRIPS4 = 0x20
 FORCE_UNITS8 = 0x40
+PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT = range(6)
 
 # Every symbol the header declares, with (restype, argtypes).
 _P = ctypes.c_void_p
@@ -45,6 +46,7 @@ SIGNATURES = {
     "my_dgemm_tune": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_D)]),
     "my_dgemm_tune_clear": (None, []),
     "my_dgemm_set_max_ctas": (_I, [_I]),
+    "my_dgemm_path": (_I, [_I, _I, ctypes.c_uint]),
     "my_dgemm_last_error": (ctypes.c_char_p, []),
     "my_dgemm_last_status": (_I, []),
     "my_dgemm_version": (ctypes.c_char_p, []),

@@ -63,19 +63,35 @@ void keep_pool_memory() {
   done.fetch_or(bit, std::memory_order_release);
 }
 
+// Which kernel a call uses (my_dgemm_path): the bandwidth kernels take the
+// shapes with one short dimension -- m == 1; m <= 8 (few rows); n == 1;
+// n <= 16 with m >= 4096 (few columns of a tall A) -- every other shape is
+// tiled.  The choice depends on (m, n) only through rules a column shard of
+// a tiled problem would NOT reproduce (n == 1, n <= 16), so sharded drivers
+// pass MY_DGEMM_FORCE_TILED exactly when the whole problem is tiled
+// (multi.py, multi_host.cu); the few-row rules depend on m alone and hold
+// for every shard.  Measurements: tools/nsmall_probe.py, tools/msmall_probe.py.
+int path_kind(int m, int n, unsigned flags) {
+  if (flags & MY_DGEMM_EXACT) return MY_DGEMM_PATH_EXACT;
+  if (!(flags & MY_DGEMM_FORCE_TILED)) {
+    if (m == 1) return MY_DGEMM_PATH_GEMV_M1;
+    if (m <= 8) return MY_DGEMM_PATH_FEW_ROWS;
+    if (n == 1) return MY_DGEMM_PATH_GEMV_N1;
+    if (n <= 16 && m >= 4096) return MY_DGEMM_PATH_FEW_COLS;
+  }
+  return MY_DGEMM_PATH_TILED;
+}
+
 // Device-pointer dispatch: picks the kernel for the shape.
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep) {
-  if (flags & MY_DGEMM_EXACT) return launch_dgemm_exact(m, n, k, A, lda, B, ldb, C, ldc, st);
-  if (!(flags & MY_DGEMM_FORCE_TILED)) {
-    if (n == 1) return launch_gemv_n1(m, k, A, lda, B, C, st, ep);
-    if (m == 1) return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st, ep);
-    // a few columns of a tall A: the bandwidth kernel (measured faster than
-    // the tiled kernel from m = 4096, tools/nsmall_probe.py)
-    if (n <= 16 && m >= 4096) return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
-    // a few rows of a wide B: its mirror (tools/msmall_probe.py)
-    if (m <= 16 && (n >= 8192 || (m <= 8 && n >= 4096)))
-      return launch_gemm_msmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
+  switch (path_kind(m, n, flags)) {
+    case MY_DGEMM_PATH_EXACT: return launch_dgemm_exact(m, n, k, A, lda, B, ldb, C, ldc, st);
+    case MY_DGEMM_PATH_GEMV_M1: return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st, ep);
+    case MY_DGEMM_PATH_FEW_ROWS: return launch_gemm_msmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
+    case MY_DGEMM_PATH_GEMV_N1: return launch_gemv_n1(m, k, A, lda, B, C, st, ep);
+    case MY_DGEMM_PATH_FEW_COLS: return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
+    default: break;
   }
   int split = (flags & MY_DGEMM_FORCE_UNITS8)    ? 8
               : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
@@ -299,6 +315,12 @@ const char *my_dgemm_last_error(void) { return t_error.c_str(); }
 int my_dgemm_last_status(void) { return t_status; }
 const char *my_dgemm_version(void) { return "paper_1609_00076_b200 0.1.0 sm_100a dmma"; }
 uint64_t my_dgemm_kernel_launches(void) { return g_launches.load(); }
+
+int my_dgemm_path(int m, int n, unsigned flags) {
+  if (m < 1) return fail(-1, "matrix dims must be positive");
+  if (n < 1) return fail(-2, "matrix dims must be positive");
+  return myd::path_kind(m, n, flags);
+}
 
 int my_dgemm_set_max_ctas(int n) {
   if (n < 0) return fail(-1, "max_ctas must be >= 0 (0 = every SM), got " + std::to_string(n));

@@ -27,6 +27,7 @@ namespace myd {
 
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep);
+int path_kind(int m, int n, unsigned flags);
 int capi_fail(int status, const std::string &msg);
 int capi_ok();
 int capi_cuda_fail(cudaError_t e, const char *where);
@@ -90,7 +91,8 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   // aligned and the bulk-copy staging path applies whatever the host ld was.
   const int64_t dlda = (m + 1) & ~1LL, dldb = (k + 1) & ~1LL, dldc = (m + 1) & ~1LL;
   const double flops = 2.0 * m * (double)n * k;
-  const bool pipelined = flops > 4e9 && n >= 1024 && m > 1 && n > 1;
+  // (the column panels and k-chunks are bitwise the one call only on the tiled path)
+  const bool pipelined = flops > 4e9 && n >= 1024 && path_kind(m, n, flags) == MY_DGEMM_PATH_TILED;
   int64_t nc0 = n, panel = n;
   if (pipelined) {
     nc0 = std::max<int64_t>(128, (n / 2) / 128 * 128);

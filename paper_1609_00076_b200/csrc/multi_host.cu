@@ -40,6 +40,7 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
                      int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep);
 int host_path(int m, int n, int k, const double *A, int lda, const double *B, int ldb, double *C, int ldc,
               unsigned flags);
+int path_kind(int m, int n, unsigned flags);
 int capi_fail(int status, const std::string &msg);
 int capi_ok();
 int capi_cuda_fail(cudaError_t e, const char *where);
@@ -156,9 +157,9 @@ void run_shard(int s, int G, Problem &P, ChunkBoard &board, ShardResult &res) {
   if (P.staged && (e = w.stage.ensure(4)) != cudaSuccess) return fail(e, "pinned staging");
   hostio::Mover mv(P.staged ? &w.stage : nullptr, w.s_up, w.s_down);
   const Epilogue ep{};
-  // Global n > 1: keep every shard on the tiled kernel (a one-column panel
-  // must not switch to the n == 1 kernel, whose summation order differs).
-  const unsigned flags = P.flags | ((P.n > 1 && P.m > 1) ? MY_DGEMM_FORCE_TILED : 0u);
+  // A tiled problem keeps every shard on the tiled kernel (a narrow panel
+  // must not switch to a bandwidth kernel, whose summation order differs).
+  const unsigned flags = P.flags | (path_kind(P.m, P.n, P.flags) == MY_DGEMM_PATH_TILED ? MY_DGEMM_FORCE_TILED : 0u);
 
   if (nloc > 0 && (e = mv.up(w.dC, P.dldc, P.C + j0 * P.ldc, P.ldc, P.m, nloc)) != cudaSuccess)
     return fail(e, "H2D C");
@@ -257,10 +258,12 @@ int multi_host_path(const int *devices, int G, int m, int n, int k, const double
   Problem P{m, n, k, A, lda, B, ldb, C, ldc, flags, (m + 1) & ~1LL, (k + 1) & ~1LL, (m + 1) & ~1LL, {}, {}, false};
   P.cols = split_columns(n, G);
   // k-chunks (multiples of 16): about two per shard, at least 256 deep.  The
-  // m == 1 / n == 1 bandwidth kernels split k their own way (their sums are
-  // not chunk-invariant): one chunk there, as the single-device call.
+  // bandwidth kernels split k their own way (their sums are not
+  // chunk-invariant): one chunk there, as the single-device call.
   const int64_t want = std::max<int64_t>(G, std::min<int64_t>(4LL * G, k / 256));
-  const int64_t kchunk = (m == 1 || n == 1) ? k : std::max<int64_t>(16, ((k + want - 1) / want + 15) / 16 * 16);
+  const int64_t kchunk = path_kind(m, n, flags) != MY_DGEMM_PATH_TILED
+                             ? k
+                             : std::max<int64_t>(16, ((k + want - 1) / want + 15) / 16 * 16);
   for (int64_t p = 0; p < k; p += kchunk) P.chunks.push_back({p, std::min<int64_t>(k, p + kchunk)});
   P.staged = !(hostio::is_pinned(A) && hostio::is_pinned(B) && hostio::is_pinned(C));
   cudaError_t e = cudaSuccess;

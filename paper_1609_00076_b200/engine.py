@@ -43,6 +43,7 @@ __all__ = [
     "my_dgemm",
     "my_dgemm_multi",
     "set_max_ctas",
+    "path",
     "dgemm_device",
     "fill_random_device",
     "operand_seed",
@@ -265,6 +266,16 @@ def max_abs_diff_device(m: int, n: int, x_ptr: int, ldx: int, y_ptr: int, ldy: i
         return mx.value, None, None
     j, i = divmod(first.value, m)
     return mx.value, i, j
+
+
+def path(m: int, n: int, exact: bool = False) -> int:
+    """Kernel family of an (m, n) call (my_dgemm_path): _capi.PATH_TILED or
+    one of the bandwidth kernels.  Sharded drivers force the tiled kernel on
+    every shard exactly when the whole problem is tiled."""
+    k = int(_capi.load().my_dgemm_path(m, n, _flags(exact)))
+    if k < 0:
+        raise ValueError(_capi.last_error())
+    return k
 
 
 def set_max_ctas(n: int) -> int:

@@ -118,10 +118,20 @@ class ShardedDgemm:
         # overlap, the default moves all of A first (one broadcast, every rank
         # waits for it) and then runs the GEMM alone; C is bitwise the same.
         self.overlap = overlap
-        # A rank whose panel is one column must not switch to the n==1 kernel
-        # when the global problem is not n==1 (keeps C identical across world
-        # sizes).
-        self.force_tiled = (plan.n > 1) if force_tiled is None else force_tiled
+        # A rank whose panel is narrow must not switch to a bandwidth kernel
+        # (n == 1, few columns) when the whole problem is tiled: every shard is
+        # forced onto the tiled kernel exactly then (keeps C identical across
+        # world sizes).  The other paths depend on m alone or keep all columns
+        # on one rank, and are not chunk-invariant: one k-chunk there.
+        if force_tiled is None:
+            from . import _capi
+            from .engine import path
+
+            force_tiled = path(plan.m, plan.n) == _capi.PATH_TILED
+            if not force_tiled and len(plan.chunks) > 1:
+                self.plan = plan = ShardPlan(plan.m, plan.n, plan.k, plan.world, plan.root, plan.columns,
+                                             ((0, plan.k),))
+        self.force_tiled = force_tiled
         self._compute = compute or self._device_compute
         self._broadcast = broadcast or self._nccl_broadcast
 

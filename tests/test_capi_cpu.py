@@ -198,3 +198,15 @@ def test_set_max_ctas_roundtrip(lib):
     assert lib.my_dgemm_set_max_ctas(-3) == -1
     assert "max_ctas" in lib.my_dgemm_last_error().decode()
     assert lib.my_dgemm_set_max_ctas(0) == 0
+
+
+@pytest.mark.parametrize("m,n,flags,want", [
+    (8192, 8192, 0, 0), (8192, 1, 0, 1), (1, 8192, 0, 2), (1, 1, 0, 2), (8192, 16, 0, 3), (4095, 16, 0, 0),
+    (8192, 17, 0, 0), (8, 8192, 0, 4), (2, 3, 0, 4), (9, 8192, 0, 0), (8, 1, 0, 4), (100, 1, 0, 1),
+    (8192, 1, 0x4, 0), (4, 4, 0x4, 0), (4, 4, 0x2, 5),
+])
+def test_path_kind_rules(lib, m, n, flags, want):
+    """my_dgemm_path: which kernel family a shape runs on (0 tiled, 1 n == 1,
+    2 m == 1, 3 few columns, 4 few rows, 5 exact; FORCE_TILED = 0x4)."""
+    assert lib.my_dgemm_path(m, n, flags) == want
+    assert lib.my_dgemm_path(0, n, flags) == -1

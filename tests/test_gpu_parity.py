@@ -435,6 +435,8 @@ def test_host_path_pageable_and_pinned_agree(torch_cuda, pinned):
     (2, 300, 1, 900, None, False),         # n == 1: the single-shard gemv, as my_dgemm
     (3, 1, 700, 500, None, False),         # m == 1
     (8, 640, 2048, 2048, None, True),
+    (3, 6, 5000, 700, (7, 703, 9), False),  # few rows: every shard on the few-row kernel
+    (2, 8192, 12, 900, None, False),       # few columns: one shard holds them all
 ])
 def test_multi_device_host_path_bitwise_equals_single(torch_cuda, shards, m, n, k, lds, pinned):
     """my_dgemm_multi_ex over `shards` column shards (all on this GPU: the
@@ -547,8 +549,9 @@ def test_c_view_8_byte_aligned_in_place(torch_cuda):
     assert float(buf[0]) == -5.5 and float(buf[-1]) == -5.5
 
 
-@pytest.mark.parametrize("world", [2, 3, 8])
-def test_sharded_step_every_world_size_bitwise_equals_single_call(torch_cuda, world):
+@pytest.mark.parametrize("world,shape", [(2, (700, 1111, 900)), (3, (700, 1111, 900)), (8, (700, 1111, 900)),
+                                         (3, (5, 3000, 400)), (2, (4096, 10, 300))])
+def test_sharded_step_every_world_size_bitwise_equals_single_call(torch_cuda, world, shape):
     """multi.ShardedDgemm's per-rank work for world sizes 2, 3, 8 run one rank
     after another on this GPU (A already resident: the broadcast is the
     identity here, no rank waits on another), C panels assembled: bitwise the
@@ -556,18 +559,19 @@ def test_sharded_step_every_world_size_bitwise_equals_single_call(torch_cuda, wo
     covers the exchange with gloo)."""
     from paper_1609_00076_b200.multi import ShardedDgemm, make_shard_plan
 
-    m, n, k = 700, 1111, 900
+    m, n, k = shape
     a, b, c, _ = dev_operands(torch_cuda, m, n, k)
     want = c.clone()
-    run_dev(torch_cuda, m, n, k, a, m, b, k, want, m, force_tiled=True)
-    got = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, want, m)  # the single call, its own path
     plan = make_shard_plan(m, n, k, world, root=0, k_chunk=256)
-    for rank in range(world):
-        j0, j1 = plan.local(rank)
-        drv = ShardedDgemm(plan, rank, broadcast=lambda t, src: None)
-        drv.step(a, m, b[j0 * k:], k, got[j0 * m:], m, broadcast_a=False)
-    torch_cuda.cuda.synchronize()
-    assert torch_cuda.equal(got, want)
+    for overlap in (False, True):  # whole-k GEMM / k-chunked GEMMs
+        got = c.clone()
+        for rank in range(world):
+            j0, j1 = plan.local(rank)
+            drv = ShardedDgemm(plan, rank, broadcast=lambda t, src: None, overlap=overlap)
+            drv.step(a, m, b[j0 * k:], k, got[j0 * m:], m, broadcast_a=False)
+        torch_cuda.cuda.synchronize()
+        assert torch_cuda.equal(got, want), overlap
 
 
 def test_device_flag_rejects_host_pointers(torch_cuda):

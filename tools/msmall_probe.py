@@ -25,8 +25,12 @@ def timed(fn, reps=10):
     return best
 
 
-for m, n, k in [(2, 8192, 8192), (4, 8192, 8192), (8, 8192, 8192), (16, 8192, 8192), (4, 100000, 2000),
-                (16, 4096, 4096), (8, 32768, 8192), (3, 5000, 777)]:
+shapes = [(2, 8192, 8192), (4, 8192, 8192), (8, 8192, 8192), (16, 8192, 8192), (4, 100000, 2000),
+          (16, 4096, 4096), (8, 32768, 8192), (3, 5000, 777), (16, 512, 4096), (8, 256, 8192), (4, 1000, 1000),
+          (16, 2048, 2048), (12, 1024, 300)]
+if len(sys.argv) > 1:
+    shapes = [tuple(int(v) for v in a.split("x")) for a in sys.argv[1:]]
+for m, n, k in shapes:
     a = torch.rand(m * k, dtype=torch.float64, device="cuda")
     b = torch.rand(k * n, dtype=torch.float64, device="cuda")
     c = torch.rand(m * n, dtype=torch.float64, device="cuda")
