@@ -116,15 +116,26 @@ __global__ void __launch_bounds__(32 * WARPS)
   int buf = 0;
   stage(kb, 0);
   __syncthreads();
-  for (int s = kb; s < ke; s += KS, buf ^= 1) {
-    if (s + KS < ke) stage(s + KS, buf ^ 1);  // next sub-chunk, behind this one's FMAs
+  // A values of the warp's KW k-steps: for NC >= 8 loaded one sub-chunk
+  // ahead, so each warp keeps a sub-chunk of HBM loads in flight while it
+  // computes (for fewer columns the extra registers cost more occupancy than
+  // the prefetch gains; tools/nsmall_probe.py)
+  constexpr bool PREFETCH = NC >= 8;
+  double av[KW][ROWS], an[KW][ROWS];
+  auto load_a = [&](int s, double (&dst)[KW][ROWS]) {
     const int pw = s + warp * KW;
-    double av[KW][ROWS];
 #pragma unroll
     for (int u = 0; u < KW; ++u)
 #pragma unroll
       for (int r = 0; r < ROWS; ++r)
-        av[u][r] = (ok[r] && pw + u < ke) ? __ldcs(a + (int64_t)(pw + u) * lda + 32 * r) : 0.0;
+        dst[u][r] = (ok[r] && pw + u < ke) ? __ldcs(a + (int64_t)(pw + u) * lda + 32 * r) : 0.0;
+  };
+  load_a(kb, av);
+  for (int s = kb; s < ke; s += KS, buf ^= 1) {
+    if (s + KS < ke) {
+      stage(s + KS, buf ^ 1);  // next sub-chunk's B, behind this one's FMAs
+      if constexpr (PREFETCH) load_a(s + KS, an);
+    }
 #pragma unroll
     for (int u = 0; u < KW; ++u) {
       const double *bp = bst + (buf * KS + warp * KW + u) * NC;
@@ -139,6 +150,14 @@ __global__ void __launch_bounds__(32 * WARPS)
       }
     }
     __syncthreads();  // buffer `buf` free, `buf ^ 1` complete
+    if constexpr (PREFETCH) {
+#pragma unroll
+      for (int u = 0; u < KW; ++u)
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) av[u][r] = an[u][r];
+    } else if (s + KS < ke) {
+      load_a(s + KS, av);
+    }
   }
   // partials of the WARPS warps per element (the B stages are no longer needed)
 #pragma unroll
