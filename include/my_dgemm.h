@@ -47,6 +47,7 @@ extern "C" {
 #define MY_DGEMM_FORCE_STRIPS2 0x10u /* run every tile as two 128x64 strips (tests) */
 #define MY_DGEMM_FORCE_STRIPS4 0x20u /* run every tile as four 128x32 strips (tests) */
 #define MY_DGEMM_FORCE_UNITS8 0x40u  /* run every tile as eight 64x32 units (tests) */
+#define MY_DGEMM_FORCE_ROWS16 0x80u  /* run every tile as eight 16x128 units (tests) */
 
 /*
  * The BASELINE.json north_star signature.  Replaces the reference's
@@ -148,7 +149,8 @@ MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, in
  * 64x32 units) on scratch device operands and remembers the fastest for
  * later calls of the same shape and operand alignment in this process.
  * Plans are bitwise-equivalent: tuning changes speed, never results.
- * out_plan: 0 heuristic, 1 full tiles, 2/4/8 units per tile.
+ * out_plan: 0 heuristic, 1 full tiles, 2/4/8 units per tile (128x64 / 128x32 /
+ * 64x32), 16 for 16x128 units.
  */
 MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan, double *out_ms);
 MY_DGEMM_API void my_dgemm_tune_clear(void);

@@ -154,7 +154,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 template <int VEC, int BM, int BN, int BKT>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
-                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
+                      int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
                       int units, int after_main, Epilogue ep) {
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
@@ -180,16 +180,24 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // Work unit u (persistent CTA b takes u = b, b + gridDim.x, ...): full
   // 128x128 tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows
   // per band, column-major inside a band), sub-block u % SPLIT of it.  With
-  // edge_ns > 0 the ragged last tile column is kept out of the raster and
-  // its units follow the raster's: per tile row, the SPLIT_M x edge_ns
-  // sub-blocks that hold valid columns (launch_dgemm_fast's edge plan).
-  // Units wholly outside C are skipped.
+  // edge = ns > 0 the ragged last tile column is kept out of the raster and
+  // its units follow the raster's: per tile row, the SPLIT_M x ns sub-blocks
+  // that hold valid columns; with edge = -ms < 0 the same for a ragged last
+  // tile row: per tile column, the ms x SPLIT_N sub-blocks holding valid rows
+  // (launch_dgemm_fast's edge plans).  Units wholly outside C are skipped.
   const int raster_units = (tiles_m * tiles_n - tile0) * SPLIT;  // units of raster tiles in this launch
+  const int edge_ns = edge > 0 ? edge : 0, edge_ms = edge < 0 ? -edge : 0;
   auto unit_origin = [&](int u, int &m0, int &n0) {
     if (edge_ns > 0 && u >= raster_units) {  // edge column: only its edge_ns valid strips per sub-row
       const int e = u - raster_units, per = SPLIT_M * edge_ns, idx = e % per;
       m0 = (e / per) * TILE_M + (idx / edge_ns) * BM;
       n0 = tiles_n * TILE_N + (idx % edge_ns) * BN;
+      return;
+    }
+    if (edge_ms > 0 && u >= raster_units) {  // edge row: only its edge_ms valid sub-rows per tile column
+      const int e = u - raster_units, per = edge_ms * SPLIT_N, idx = e % per;
+      m0 = tiles_m * TILE_M + (idx / SPLIT_N) * BM;
+      n0 = (e / per) * TILE_N + (idx % SPLIT_N) * BN;
       return;
     }
     const int tile = tile0 + u / SPLIT, sub = u % SPLIT;
@@ -564,7 +572,7 @@ bool pdl_enabled() {
 template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>()>
 cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                        const double *B,
-                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
+                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
                        int after_main, cudaStream_t st) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
@@ -593,7 +601,7 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK>, M, N, K, A, lda, B, ldb, C, ldc,
-                                     tiles_m, tiles_n, tile0, edge_ns, (int)units, after_main, ep);
+                                     tiles_m, tiles_n, tile0, edge, (int)units, after_main, ep);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -601,19 +609,21 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
 
 template <int VEC>
 cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
-                         const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge_ns,
+                         const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
                          int after_main,
                          cudaStream_t st) {
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
         if (K >= 1024)  // long K: deeper slabs, fewer ring handshakes
-          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
+          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
       }
-      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
-    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
-    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
-    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge_ns, after_main, st);
+      return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+    case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+    case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+    case 16:  // 16x128 units (8 per tile, stacked in m): few-row problems and ragged last tile rows
+      return launch_one<VEC, 16, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+    default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
   }
 }
 
@@ -651,9 +661,11 @@ int set_max_ctas(int n) { return g_max_ctas.exchange(n); }
 // (tools/plan_probe.py, profiles/plan_probe_r01.log): a unit of s-th of a
 // tile at depth K takes ideal/e_s + b_s microseconds on one SM (ideal at
 // 128 flop/clk, 1.965 GHz), and a second launch costs ~15 us; the cheapest
-// wins.  force_split pins the plan (tests and the tuner): 0 = heuristic,
-// 1 = full tiles only, 2 / 4 / 8 = every tile as units.  Every plan
-// computes bitwise the same C.
+// wins.  A ragged last tile row (M mod 128 in 1..64, and problems of <= 64
+// rows) gets the same treatment as a ragged column, with 64x32 or 16x128
+// units.  force_split pins the plan (tests and the tuner): 0 = heuristic,
+// 1 = full tiles only, 2 / 4 / 8 / 16 = every tile as 128x64 / 128x32 /
+// 64x32 / 16x128 units.  Every plan computes bitwise the same C.
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -664,20 +676,22 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   const bool vec2 =
       !force_vec1 && (lda % 2 == 0) && (ldb % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
   const long long G = sm_count();
-  int raster_n = tiles_n;  // tile columns in the grouped raster (the rest: edge column, appended)
-  int edge_ns = 0;         // edge plan: valid BN-wide strips of the edge column
+  int raster_m = tiles_m, raster_n = tiles_n;  // tile rows / columns in the grouped raster
+  int edge = 0;  // edge plans: > 0 valid strips of a separate last tile column, < 0 sub-rows of a last row
   long long q = tiles / G;  // full-tile rounds of the main launch
-  int split = 1;
+  int split = 1;            // 1 full tiles; 2 / 4 / 8 units 128x64 / 128x32 / 64x32; 16 units 16x128
+  auto per_tile = [](int s) { return s == 16 ? 8 : s; };
   if (force_split > 1) {
-    split = force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2);  // every tile as units
+    split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
     q = 0;
   } else if (force_split == 0) {
     auto unit_us = [&](int s) {  // one unit of 1/s tile, depth K, on one SM (fitted)
-      const double ideal = 2.0 * TILE_M * TILE_N / s * K / 251.5e3;
+      const double ideal = 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3;
       switch (s) {
         case 1: return ideal / 0.990 + 2.8;
         case 2: return ideal / 0.984 + 7.2;
         case 4: return ideal / 0.983 + 4.4;
+        case 16: return ideal / 0.970 + 2.0;
         default: return ideal / 0.977 + 2.0;
       }
     };
@@ -714,28 +728,51 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         if (cost < best - 1e-9) {
           best = cost;
           split = s;
+          raster_m = tiles_m;
           raster_n = tiles_n - 1;
-          edge_ns = ns;
+          edge = ns;
+          q = qe;
+        }
+      }
+    }
+    const int rem_m = M % TILE_M;
+    if (rem_m >= 1 && rem_m <= 64) {  // ragged last tile row (or a problem < 64 rows) out of the raster
+      const long long te = (long long)(tiles_m - 1) * tiles_n;
+      const long long qe = te / G, re = te % G;
+      for (int s : {8, 16}) {
+        const int ms = s == 8 ? 1 : (rem_m + 15) / 16;  // 64x32: 1 sub-row (x 4 strips); 16x128: 16-row sub-rows
+        const long long nonempty = re * per_tile(s) + (long long)tiles_n * ms * (s == 8 ? 4 : 1);
+        const double cost =
+            (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
+        if (cost < best - 1e-9) {
+          best = cost;
+          split = s;
+          raster_m = tiles_m - 1;
+          raster_n = tiles_n;
+          edge = -ms;
           q = qe;
         }
       }
     }
   }
-  const long long raster_tiles = (long long)tiles_m * raster_n;
+  const long long raster_tiles = (long long)raster_m * raster_n;
   const long long main_tiles = split == 1 ? tiles : q * G;
   cudaError_t e = cudaSuccess;
   if (main_tiles > 0)
-    e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
+    e = vec2 ? launch_split<2>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, raster_m, raster_n, 0, 0,
                                0, stream)
-             : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n, 0, 0,
+             : launch_split<1>(ep, 1, (unsigned)main_tiles, M, N, K, A, lda, B, ldb, C, ldc, raster_m, raster_n, 0, 0,
                                0, stream);
   if (e != cudaSuccess || split == 1) return e;
-  const long long edge_units = edge_ns > 0 ? (long long)tiles_m * (split == 8 ? 2 : 1) * edge_ns : 0;
-  const unsigned units = (unsigned)((raster_tiles - main_tiles) * split + edge_units);
-  return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
-                                (int)main_tiles, edge_ns, main_tiles > 0, stream)
-              : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, raster_n,
-                                (int)main_tiles, edge_ns, main_tiles > 0, stream);
+  long long edge_units = 0;
+  if (edge > 0) edge_units = (long long)tiles_m * (split == 8 ? 2 : 1) * edge;
+  if (edge < 0) edge_units = (long long)tiles_n * (-edge) * (split == 8 ? 4 : 1);
+  const long long raster_left = edge == 0 ? tiles - main_tiles : raster_tiles - main_tiles;
+  const unsigned units = (unsigned)(raster_left * per_tile(split) + edge_units);
+  return vec2 ? launch_split<2>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, raster_m, raster_n,
+                                (int)main_tiles, edge, main_tiles > 0, stream)
+              : launch_split<1>(ep, split, units, M, N, K, A, lda, B, ldb, C, ldc, raster_m, raster_n,
+                                (int)main_tiles, edge, main_tiles > 0, stream);
 }
 
 }  // namespace myd

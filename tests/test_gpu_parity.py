@@ -200,13 +200,17 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
     (2304, 2304, 128, 2304, 128, 2304),     # plan picks tail strips (324 tiles)
     (4093, 4099, 200, 4100, 202, 4096),     # ragged last tile column run as tail strips (edge plan)
     (1500, 2050, 160, 1500, 160, 1503),     # edge plan, odd ldc, 2 valid columns in the edge tile
+    (4100, 3000, 200, 4100, 200, 4100),     # ragged last tile row (4 rows) run as 16x128 units
+    (12, 9000, 500, 13, 500, 12),           # 9..16 rows: tiled, 16x128 units only
+    (2100, 777, 300, 2101, 301, 2103),      # ragged row (52 rows) and column, odd lds
 ])
 def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
-    """Full tiles, 128x64 strips, 128x32 strips and 64x32 units give bitwise
-    the same C (the per-element DMMA sequence does not depend on the CTA shape)."""
+    """Full tiles, 128x64 strips, 128x32 strips, 64x32 and 16x128 units and
+    the heuristic's edge plans give bitwise the same C (the per-element DMMA
+    sequence does not depend on the CTA shape)."""
     a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
     outs = []
-    for strips in (0, 2, 4, 8):
+    for strips in (0, 2, 4, 8, 16):
         cc = c.clone()
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips)
         outs.append(cc)
