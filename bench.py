@@ -301,7 +301,7 @@ def run_b200_arm(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         engine.dgemm_device(mm, nl, kc, A_.data_ptr(), lda, B_.data_ptr(), ldb, C_.data_ptr(), ldc,
-                            st, force_tiled=drv.force_tiled)
+                            st, path=drv.path)
         e1.record(stream)
         launch_events.append((e0, e1, kc))
 
@@ -421,7 +421,7 @@ def measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total):
 
     def call():
         _capi.check(lib.my_dgemm_ex(m, nloc, k, hA.data_ptr(), m, hB.data_ptr(), k, hC.data_ptr(), m,
-                                    _capi.FORCE_TILED if world > 1 else 0, None))
+                                    _capi.FORCE_PATH(engine.path(m, n_total, False)), None))
 
     for _ in range(2):
         call()

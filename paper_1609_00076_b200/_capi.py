@@ -25,6 +25,10 @@ FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
 PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT = range(6)
 
+
+def FORCE_PATH(p: int) -> int:  # noqa: N802 - mirrors the C macro
+    return (p + 1) << 8
+
 # Every symbol the header declares, with (restype, argtypes).
 _P = ctypes.c_void_p
 _I = ctypes.c_int

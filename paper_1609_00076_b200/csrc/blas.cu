@@ -23,6 +23,7 @@ namespace myd {
 cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                      int64_t ldc, cudaStream_t st, unsigned flags, const Epilogue &ep);
 int capi_fail(int status, const std::string &msg);
+bool path_fits(int m, int n, unsigned flags);
 int capi_ok();
 int capi_cuda_fail(cudaError_t e, const char *where);
 void keep_pool_memory();
@@ -139,8 +140,11 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
     return capi_fail(-13, buf);
   }
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
-                         MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8;
+                         MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
+                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_PATH_MASK;
   if (flags & ~known) return capi_fail(-14, "unknown flag bits");
+  if (m > 0 && n > 0 && !path_fits(m, n, flags))
+    return capi_fail(-14, "MY_DGEMM_FORCE_PATH does not suit the shape");
   if ((flags & MY_DGEMM_EXACT) && !(alpha == 1.0 && beta == 1.0))
     return capi_fail(-14, "MY_DGEMM_EXACT needs alpha == 1 and beta == 1 (the reference oracle's operation)");
   // quick return (reference BLAS)

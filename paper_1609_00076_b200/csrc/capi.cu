@@ -64,22 +64,34 @@ void keep_pool_memory() {
 }
 
 // Which kernel a call uses (my_dgemm_path): the bandwidth kernels take the
-// shapes with one short dimension -- m == 1; m <= 8 (few rows); n == 1;
-// n <= 16 with m >= 4096 (few columns of a tall A) -- every other shape is
-// tiled.  The choice depends on (m, n) only through rules a column shard of
-// a tiled problem would NOT reproduce (n == 1, n <= 16), so sharded drivers
-// pass MY_DGEMM_FORCE_TILED exactly when the whole problem is tiled
-// (multi.py, multi_host.cu); the few-row rules depend on m alone and hold
-// for every shard.  Measurements: tools/nsmall_probe.py, tools/msmall_probe.py.
+// shapes with one short dimension -- m == 1; few rows (m <= 4 with
+// n <= 16384, m <= 8 with n <= 4096: beyond that the tiled kernel's 16x128
+// units win); n == 1; few columns (n <= 16 with m >= 4096) -- every other
+// shape is tiled.  Sharded drivers pass the whole problem's path to every
+// shard (MY_DGEMM_FORCE_PATH), so a narrow shard never changes kernel.
+// Measurements: tools/nsmall_probe.py, tools/msmall_probe.py.
 int path_kind(int m, int n, unsigned flags) {
   if (flags & MY_DGEMM_EXACT) return MY_DGEMM_PATH_EXACT;
-  if (!(flags & MY_DGEMM_FORCE_TILED)) {
-    if (m == 1) return MY_DGEMM_PATH_GEMV_M1;
-    if (m <= 8) return MY_DGEMM_PATH_FEW_ROWS;
-    if (n == 1) return MY_DGEMM_PATH_GEMV_N1;
-    if (n <= 16 && m >= 4096) return MY_DGEMM_PATH_FEW_COLS;
-  }
+  if (flags & MY_DGEMM_PATH_MASK) return (int)((flags & MY_DGEMM_PATH_MASK) >> 8) - 1;
+  if (flags & MY_DGEMM_FORCE_TILED) return MY_DGEMM_PATH_TILED;
+  if (m == 1) return MY_DGEMM_PATH_GEMV_M1;
+  if ((m <= 4 && n <= 16384) || (m <= 8 && n <= 4096)) return MY_DGEMM_PATH_FEW_ROWS;
+  if (n == 1) return MY_DGEMM_PATH_GEMV_N1;
+  if (n <= 16 && m >= 4096) return MY_DGEMM_PATH_FEW_COLS;
   return MY_DGEMM_PATH_TILED;
+}
+
+// A forced path must suit the shape.
+bool path_fits(int m, int n, unsigned flags) {
+  if (!(flags & MY_DGEMM_PATH_MASK)) return true;
+  switch ((int)((flags & MY_DGEMM_PATH_MASK) >> 8) - 1) {
+    case MY_DGEMM_PATH_TILED: return true;
+    case MY_DGEMM_PATH_GEMV_N1: return n == 1;
+    case MY_DGEMM_PATH_GEMV_M1: return m == 1;
+    case MY_DGEMM_PATH_FEW_COLS: return n <= 16;
+    case MY_DGEMM_PATH_FEW_ROWS: return m <= 16;
+    default: return false;
+  }
 }
 
 // Device-pointer dispatch: picks the kernel for the shape.
@@ -225,8 +237,9 @@ int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, 
   if (v) return v;
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
-                         MY_DGEMM_FORCE_ROWS16;
+                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_PATH_MASK;
   if (flags & ~known) return fail(-10, "unknown flag bits");
+  if (!path_fits(m, n, flags)) return fail(-10, "MY_DGEMM_FORCE_PATH does not suit the shape");
   if (flags & MY_DGEMM_DEVICE_PTRS) {
     // A host pointer here would fault the GPU; reject it as an argument error.
     const void *ptrs[3] = {A, B, C};
@@ -321,6 +334,7 @@ uint64_t my_dgemm_kernel_launches(void) { return g_launches.load(); }
 int my_dgemm_path(int m, int n, unsigned flags) {
   if (m < 1) return fail(-1, "matrix dims must be positive");
   if (n < 1) return fail(-2, "matrix dims must be positive");
+  if (!path_fits(m, n, flags)) return fail(-3, "MY_DGEMM_FORCE_PATH does not suit the shape");
   return myd::path_kind(m, n, flags);
 }
 

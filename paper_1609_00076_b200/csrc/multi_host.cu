@@ -157,9 +157,9 @@ void run_shard(int s, int G, Problem &P, ChunkBoard &board, ShardResult &res) {
   if (P.staged && (e = w.stage.ensure(4)) != cudaSuccess) return fail(e, "pinned staging");
   hostio::Mover mv(P.staged ? &w.stage : nullptr, w.s_up, w.s_down);
   const Epilogue ep{};
-  // A tiled problem keeps every shard on the tiled kernel (a narrow panel
-  // must not switch to a bandwidth kernel, whose summation order differs).
-  const unsigned flags = P.flags | (path_kind(P.m, P.n, P.flags) == MY_DGEMM_PATH_TILED ? MY_DGEMM_FORCE_TILED : 0u);
+  // Every shard runs the whole problem's kernel family (a narrow panel must
+  // not switch kernels: their summation orders differ).
+  const unsigned flags = P.flags | MY_DGEMM_FORCE_PATH(path_kind(P.m, P.n, P.flags));
 
   if (nloc > 0 && (e = mv.up(w.dC, P.dldc, P.C + j0 * P.ldc, P.ldc, P.m, nloc)) != cudaSuccess)
     return fail(e, "H2D C");

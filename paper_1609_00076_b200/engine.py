@@ -129,8 +129,10 @@ def check_conformal(a, b, c) -> tuple[int, int, int]:
     return a.m, b.n, a.n
 
 
-def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, strips: int = 0) -> int:
+def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, strips: int = 0,
+           path: int | None = None) -> int:
     f = _capi.EXACT if exact else 0
+    f |= _capi.FORCE_PATH(path) if path is not None else 0
     f |= _capi.FORCE_TILED if force_tiled else 0
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
     f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
@@ -232,13 +234,14 @@ def my_dgemm_multi(devices, m: int, n: int, k: int, A: np.ndarray, lda: int, B: 
 
 def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int, ldc: int,
                  stream: int = 0, exact: bool = False, force_tiled: bool = False,
-                 force_vec1: bool = False, strips: int = 0) -> None:
+                 force_vec1: bool = False, strips: int = 0, path: int | None = None) -> None:
     """Raw device-pointer call (asynchronous on `stream`).  `strips` (2 or 4)
-    forces every tile through the narrow-strip kernels, 8 through the 64x32
-    units (tests)."""
+    forces every tile through the narrow-strip kernels, 8 / 16 through the
+    64x32 / 16x128 units (tests); `path` forces a kernel family
+    (_capi.PATH_*, what sharded drivers pass to every shard)."""
     lib = _capi.load()
     _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
-                                _flags(exact, force_tiled, force_vec1, strips) | _capi.DEVICE_PTRS,
+                                _flags(exact, force_tiled, force_vec1, strips, path) | _capi.DEVICE_PTRS,
                                 ctypes.c_void_p(stream)))
 
 

@@ -118,20 +118,18 @@ class ShardedDgemm:
         # overlap, the default moves all of A first (one broadcast, every rank
         # waits for it) and then runs the GEMM alone; C is bitwise the same.
         self.overlap = overlap
-        # A rank whose panel is narrow must not switch to a bandwidth kernel
-        # (n == 1, few columns) when the whole problem is tiled: every shard is
-        # forced onto the tiled kernel exactly then (keeps C identical across
-        # world sizes).  The other paths depend on m alone or keep all columns
-        # on one rank, and are not chunk-invariant: one k-chunk there.
-        if force_tiled is None:
-            from . import _capi
-            from .engine import path
+        # Every rank runs the whole problem's kernel family (a narrow panel
+        # must not switch kernels: their summation orders differ), which keeps
+        # C identical across world sizes.  Only the tiled family is bitwise
+        # k-chunk invariant: the other paths get one k-chunk.
+        from . import _capi
+        from .engine import path as path_of
 
-            force_tiled = path(plan.m, plan.n) == _capi.PATH_TILED
-            if not force_tiled and len(plan.chunks) > 1:
-                self.plan = plan = ShardPlan(plan.m, plan.n, plan.k, plan.world, plan.root, plan.columns,
-                                             ((0, plan.k),))
-        self.force_tiled = force_tiled
+        self.path = _capi.PATH_TILED if force_tiled else path_of(plan.m, plan.n)
+        if self.path != _capi.PATH_TILED and len(plan.chunks) > 1:
+            self.plan = plan = ShardPlan(plan.m, plan.n, plan.k, plan.world, plan.root, plan.columns,
+                                         ((0, plan.k),))
+        self.force_tiled = self.path == _capi.PATH_TILED
         self._compute = compute or self._device_compute
         self._broadcast = broadcast or self._nccl_broadcast
 
@@ -142,7 +140,7 @@ class ShardedDgemm:
         from .engine import dgemm_device
 
         dgemm_device(m, nloc, kc, A.data_ptr(), lda, B.data_ptr(), ldb, C.data_ptr(), ldc,
-                     torch.cuda.current_stream().cuda_stream, force_tiled=self.force_tiled)
+                     torch.cuda.current_stream().cuda_stream, path=self.path)
 
     def _nccl_broadcast(self, tensor, src):
         import torch.distributed as dist

@@ -554,7 +554,8 @@ def test_c_view_8_byte_aligned_in_place(torch_cuda):
 
 
 @pytest.mark.parametrize("world,shape", [(2, (700, 1111, 900)), (3, (700, 1111, 900)), (8, (700, 1111, 900)),
-                                         (3, (5, 3000, 400)), (2, (4096, 10, 300))])
+                                         (3, (5, 3000, 400)), (2, (4096, 10, 300)), (3, (8, 8192, 300)),
+                                         (2, (3, 20000, 64))])
 def test_sharded_step_every_world_size_bitwise_equals_single_call(torch_cuda, world, shape):
     """multi.ShardedDgemm's per-rank work for world sizes 2, 3, 8 run one rank
     after another on this GPU (A already resident: the broadcast is the
