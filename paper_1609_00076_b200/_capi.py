@@ -23,6 +23,7 @@ FORCE_STRIPS2 = 0x10
 FORCE_STRIPS4 = 0x20
 FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
+FORCE_STREAMK = 0x800
 PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT = range(6)
 
 

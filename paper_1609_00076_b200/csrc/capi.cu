@@ -105,7 +105,8 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     case MY_DGEMM_PATH_FEW_COLS: return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
     default: break;
   }
-  int split = (flags & MY_DGEMM_FORCE_ROWS16)    ? 16
+  int split = (flags & MY_DGEMM_FORCE_STREAMK)   ? 32
+              : (flags & MY_DGEMM_FORCE_ROWS16)  ? 16
               : (flags & MY_DGEMM_FORCE_UNITS8)  ? 8
               : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
               : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
@@ -237,7 +238,7 @@ int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, 
   if (v) return v;
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
-                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_PATH_MASK;
+                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_FORCE_STREAMK | MY_DGEMM_PATH_MASK;
   if (flags & ~known) return fail(-10, "unknown flag bits");
   if (!path_fits(m, n, flags)) return fail(-10, "MY_DGEMM_FORCE_PATH does not suit the shape");
   if (flags & MY_DGEMM_DEVICE_PTRS) {

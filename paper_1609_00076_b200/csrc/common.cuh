@@ -133,6 +133,20 @@ struct Epilogue {
   int blas = 0;
 };
 
+// Stream-K schedule of the tiled kernel (iters == 0: unit mode): the first
+// dp_tiles tiles run as whole tiles round-robin (data-parallel rounds), then
+// the (tile, slab) iterations of the tiles from tile0 on -- `iters` of them --
+// are split evenly over the grid; partial accumulators of cut tiles in `work`
+// (one slot per CTA), per-(slot, warp) flags set to `epoch`.
+struct StreamK {
+  long long dp_tiles = 0;  // whole tiles [0, dp_tiles) first, round-robin
+  long long tile0 = 0;     // first tile of the stream-K phase
+  long long iters = 0;
+  double *work = nullptr;
+  unsigned long long *flags = nullptr;
+  unsigned long long epoch = 0;
+};
+
 // Kernel launch counter shared by every launcher (my_dgemm_kernel_launches).
 void count_launch(int n = 1);
 

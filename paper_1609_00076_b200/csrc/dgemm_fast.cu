@@ -151,11 +151,11 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT>
+template <int VEC, int BM, int BN, int BKT, bool SKM>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
-                      int units, int after_main, Epilogue ep) {
+                      int units, int after_main, StreamK sk, Epilogue ep) {
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
   constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
@@ -222,10 +222,79 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int KT = (K + BK - 1) / BK;
-#ifdef MYD_TIMELINE
-  int unit_ord = 0;
-  if (tid == 0) atomicMin(&g_tl[0], gtimer());
-#endif
+
+  // Work segments.  Unit mode (sk.iters == 0): unit u, all K slabs, from C to
+  // C.  Stream-K mode (full tiles only): tiles [0, dp_tiles) run whole,
+  // round-robin (data-parallel rounds: co-running tiles stay neighbours in
+  // the raster, sharing A/B panels in L2); the remaining tiles' (tile, slab)
+  // iterations are split evenly over the CTAs.  Within a tile the iterations
+  // are numbered by DESCENDING slab, so a tile cut between CTA b (end of its
+  // range) and b + 1 (start of its range) leaves CTA b + 1 -- which gets
+  // there first -- the LOWER slabs, from C to a partial accumulator written
+  // to workspace slot b, and CTA b the UPPER slabs, from that partial to C.
+  // Each segment runs its slabs in ascending order, so every element sees
+  // exactly the DMMA chain of one CTA doing the whole K: bitwise the same C,
+  // without the last round's quantisation.  The stream-K phase spans at
+  // least one tile per CTA, so a tile is cut at most once, and CTA b only
+  // ever waits for CTA b + 1's first segment (which waits on nothing): no
+  // deadlock.  Cursor: < SK0 a data-parallel tile, else SK0 + iteration.
+  struct Seg {
+    int m0, n0, kb, ke, slot;
+    bool from_c, to_c;
+  };
+  constexpr int SK0 = 1 << 30;  // stream-K cursors (the planner keeps iterations < 2^30)
+  const int sk_iters = (int)sk.iters, sk_dp = (int)sk.dp_tiles;
+  const int sk_per = sk_iters / (int)gridDim.x, sk_rem = sk_iters % (int)gridDim.x;
+  const int sk_lo = sk_per * (int)blockIdx.x + min((int)blockIdx.x, sk_rem);
+  const int sk_hi = sk_lo + sk_per + ((int)blockIdx.x < sk_rem ? 1 : 0);
+  auto seg_at = [&](int cur, Seg &sg) -> bool {
+    if constexpr (!SKM) {
+      if (cur >= units) return false;
+      unit_origin(cur, sg.m0, sg.n0);
+      sg.kb = 0;
+      sg.ke = KT;
+      sg.from_c = sg.to_c = true;
+      sg.slot = -1;
+      return true;
+    } else {
+      if (cur < SK0) {  // data-parallel tile
+        unit_origin(cur, sg.m0, sg.n0);
+        sg.kb = 0;
+        sg.ke = KT;
+        sg.from_c = sg.to_c = true;
+        sg.slot = -1;
+        return true;
+      }
+      const int it = cur - SK0;
+      if (it >= sk_hi) return false;
+      const int t = it / KT, l0 = it - t * KT;
+      const int l1 = min(KT, sk_hi - t * KT);
+      unit_origin((int)sk.tile0 + t, sg.m0, sg.n0);
+      sg.kb = KT - l1;
+      sg.ke = KT - l0;
+      sg.from_c = sg.kb == 0;
+      sg.to_c = sg.ke == KT;
+      sg.slot = sg.to_c ? (int)blockIdx.x : (int)blockIdx.x - 1;  // upper part reads b; lower part writes b - 1
+      return true;
+    }
+  };
+  auto seg_first = [&]() -> int {
+    if constexpr (!SKM) {
+      return next_unit(blockIdx.x);
+    } else {
+      return (int)blockIdx.x < sk_dp ? (int)blockIdx.x : SK0 + sk_lo;
+    }
+  };
+  auto seg_next = [&](int cur, const Seg &sg) -> int {
+    if constexpr (!SKM) {
+      return next_unit(cur + gridDim.x);
+    } else {
+      if (cur < SK0) return cur + (int)gridDim.x < sk_dp ? cur + (int)gridDim.x : SK0 + sk_lo;
+      const int it = cur - SK0;
+      return SK0 + (it / KT) * KT + (KT - sg.kb);
+    }
+  };
+
 
   if (tid == 0) {
 #pragma unroll
@@ -259,18 +328,21 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
 #endif
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
-    int u = next_unit(blockIdx.x), m0 = 0, n0 = 0;
-    if (u < units) unit_origin(u, m0, n0);  // integer work, overlapping the previous grid's drain
+    int cur = seg_first();
+    Seg sg;
+    bool have = seg_at(cur, sg);  // integer work, overlapping the previous grid's drain
     if (!after_main) asm volatile("griddepcontrol.wait;\n" "griddepcontrol.launch_dependents;\n" ::: "memory");
-    for (; u < units; u = next_unit(u + gridDim.x), unit_origin(u < units ? u : 0, m0, n0)) {
+    bool first_seg = true;
+    for (; have; cur = seg_next(cur, sg), have = seg_at(cur, sg), first_seg = false) {
+      const int m0 = sg.m0, n0 = sg.n0;
 #ifdef MYD_TIMELINE
-      if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[9] = gtimer();
+      if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg) g_tl[9] = gtimer();
 #endif
       // C block of the unit through CS ring slots (my_dgemm contract only:
       // the BLAS epilogue reads C at the end instead).  The copies are issued
       // while the consumers finish the previous unit, so the C load is off the
       // critical path and spread in time instead of bursting at unit start.
-      if (!ep.blas) {
+      if (!ep.blas && sg.from_c) {
         const bool c_bulk = c_aligned && (m0 + BM <= M) && (n0 + BN <= N);
         for (int cs = 0; cs < CS; ++cs, ++g) {
           const int slot = g % STAGES;
@@ -304,7 +376,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, rows * 8, &full_bar[slot]);
           }
 #ifdef MYD_TIMELINE
-          if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x) g_tl[10 + cs] = gtimer();
+          if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg) g_tl[10 + cs] = gtimer();
 #endif
         }
       }
@@ -312,7 +384,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // engine straight into the padded slab layout, with no LSU traffic.
       // Edge units and a ragged last slab use zero-filling LDGSTS.
       const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
-      for (int kt = 0; kt < KT; ++kt, ++g) {
+      for (int kt = sg.kb; kt < sg.ke; ++kt, ++g) {
         const int slot = g % STAGES;
         if (g >= STAGES) {
           PROF_T0();
@@ -339,7 +411,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
           }
 #ifdef MYD_TIMELINE
-          if (blockIdx.x == 0 && pw == 0 && lane == 0 && u == (int)blockIdx.x && kt == 0) g_tl[7] = gtimer();
+          if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg && kt == sg.kb) g_tl[7] = gtimer();
 #endif
           continue;
         }
@@ -456,19 +528,61 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (lane == 0) PROF_ADD(6, clock64() - c_t0);
 #endif
   };
-  uint32_t g = 0;       // ring position (C blocks and slabs consumed so far)
-  int u_next = next_unit(blockIdx.x);
-  if (u_next < units) load_c_block(0);
-  for (int u = u_next; u < units; u = u_next, g += KT) {
-    u_next = next_unit(u + gridDim.x);
-    int m0, n0;
-    unit_origin(u, m0, n0);
-    // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
-    // thread's pair is two consecutive rows of one column: 16 contiguous
-    // bytes in column-major C):  acc[i][j][e] = C(row0 + 8i + e, col0 + 8j).
-    const int row0 = m0 + wm * WM + 2 * q;
-    const int col0 = n0 + wn * WN + r;
-    if (!ep.blas) g += CS;  // this unit's C block (already in acc)
+  // Stream-K partial accumulators: workspace slot s, warp w holds this
+  // warp's FM x FN x 2 values as double2 [v][lane] (coalesced); the flag of
+  // (s, w) carries the launch's epoch once they are written.
+  constexpr int NV2 = FM * FN;  // double2 per lane
+  auto part_base = [&](int slot) -> double2 * {
+    return reinterpret_cast<double2 *>(sk.work) + ((int64_t)slot * CONSUMER_WARPS + warp) * NV2 * 32 + lane;
+  };
+  auto store_partial = [&](int slot) {
+    double2 *p = part_base(slot);
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) __stcg(p + (i * FN + j) * 32, make_double2(acc[i][j][0], acc[i][j][1]));
+    __threadfence();
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(sk.flags + slot * CONSUMER_WARPS + warp),
+                   "l"(sk.epoch)
+                   : "memory");
+  };
+  auto load_partial = [&](int slot) {
+    const unsigned long long *f = sk.flags + slot * CONSUMER_WARPS + warp;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(f) : "memory");
+      if (v == sk.epoch) break;
+      __nanosleep(64);
+    }
+    const double2 *p = part_base(slot);
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const double2 v = __ldcg(p + (i * FN + j) * 32);
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
+      }
+  };
+  // accumulator initialisation of a segment whose C block (if any) sits at
+  // ring position gpos; returns the ring position of its first slab
+  auto init_acc = [&](const Seg &sg, uint32_t gpos) -> uint32_t {
+    if (!sg.from_c) {
+      load_partial(sg.slot);
+      return gpos;
+    }
+    load_c_block(gpos);
+    return ep.blas ? gpos : gpos + CS;
+  };
+  uint32_t g = 0;  // ring position (C blocks and slabs consumed so far)
+  int cur = seg_first();
+  Seg sg;
+  bool have = seg_at(cur, sg);
+  if (have) g = init_acc(sg, 0);
+  while (have) {
+    const int NS = sg.ke - sg.kb;
     TL_MARK(3);
 #ifdef MYD_FAST_PROFILE
     long long loop_t0 = clock64();
@@ -480,7 +594,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       TL_MARK(4);
     }
     load_frags(0, g % STAGES, 0);
-    for (int kt = 0; kt < KT; ++kt) {
+    for (int kt = 0; kt < NS; ++kt) {
       const uint32_t gs = g + kt;
       const int slot = gs % STAGES;
       const int nslot = (gs + 1) % STAGES;
@@ -488,12 +602,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       bool next_ready = true;
 #pragma unroll
       for (int kk = 0; kk < KSTEPS; ++kk) {
-        const int cur = kk & 1;
+        const int cur_buf = kk & 1;
         // Probe the next slab's barrier early; its latency hides behind DMMAs.
-        if (kk == PROBE_STEP && kt + 1 < KT) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
+        if (kk == PROBE_STEP && kt + 1 < NS) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
         if (kk + 1 < KSTEPS) {
-          load_frags(cur ^ 1, slot, kk + 1);
-        } else if (kt + 1 < KT) {
+          load_frags(cur_buf ^ 1, slot, kk + 1);
+        } else if (kt + 1 < NS) {
           if (!next_ready) {
             PROF_T0();
             mbar_wait(&full_bar[nslot], nparity);
@@ -502,12 +616,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
               PROF_ADD(1, 1);
             }
           }
-          load_frags(cur ^ 1, nslot, 0);
+          load_frags(cur_buf ^ 1, nslot, 0);
         }
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
-          for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fb[cur][j], fa[cur][i]);
+          for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fb[cur_buf][j], fa[cur_buf][i]);
       }
       // every fragment of this slab has been consumed by an issued DMMA
       __syncwarp();
@@ -521,40 +635,58 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     }
 #endif
     TL_MARK(5);
-    // ---- epilogue: valid region only (padding rows never touched) ----
-    const bool has_next = u_next < units;
-    const bool vec_store = c_aligned;
+    // the next segment (worked out after the K loop: nothing extra stays live in it)
+    const int ncur = seg_next(cur, sg);
+    Seg nsg;
+    const bool has_next = seg_at(ncur, nsg);
+    if (!sg.to_c) {
+      store_partial(sg.slot);  // the lower slabs of a tile another CTA finishes
+    } else {
+      // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
+      // thread's pair is two consecutive rows of one column: 16 contiguous
+      // bytes in column-major C):  acc[i][j][e] = C(row0 + 8i + e, col0 + 8j).
+      const int row0 = sg.m0 + wm * WM + 2 * q;
+      const int col0 = sg.n0 + wn * WN + r;
+      // ---- epilogue: valid region only (padding rows never touched) ----
+      const bool vec_store = c_aligned;
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j) {
-        const int row = row0 + i * 8, col = col0 + j * 8;
-        if (col >= N || row >= M) continue;
-        double *cp = C + (int64_t)col * ldc + row;
-        double v0 = acc[i][j][0], v1 = acc[i][j][1];
-        const bool pair = row + 1 < M;
-        if (ep.blas) {  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
-          v0 = ep.beta == 0.0 ? ep.alpha * v0 : fma(ep.alpha, v0, ep.beta * cp[0]);
-          if (pair) v1 = ep.beta == 0.0 ? ep.alpha * v1 : fma(ep.alpha, v1, ep.beta * cp[1]);
+        for (int j = 0; j < FN; ++j) {
+          const int row = row0 + i * 8, col = col0 + j * 8;
+          if (col >= N || row >= M) continue;
+          double *cp = C + (int64_t)col * ldc + row;
+          double v0 = acc[i][j][0], v1 = acc[i][j][1];
+          const bool pair = row + 1 < M;
+          if (ep.blas) {  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
+            v0 = ep.beta == 0.0 ? ep.alpha * v0 : fma(ep.alpha, v0, ep.beta * cp[0]);
+            if (pair) v1 = ep.beta == 0.0 ? ep.alpha * v1 : fma(ep.alpha, v1, ep.beta * cp[1]);
+          }
+          if (pair && vec_store) {
+            *reinterpret_cast<double2 *>(cp) = make_double2(v0, v1);
+          } else {
+            cp[0] = v0;
+            if (pair) cp[1] = v1;
+          }
         }
-        if (pair && vec_store) {
-          *reinterpret_cast<double2 *>(cp) = make_double2(v0, v1);
-        } else {
-          cp[0] = v0;
-          if (pair) cp[1] = v1;
-        }
-      }
-    if (has_next) load_c_block(g + KT);
+    }
+    g += NS;
+    if (has_next) g = init_acc(nsg, g);
     TL_MARK(6);
 #ifdef MYD_TIMELINE
     ++unit_ord;
 #endif
+    cur = ncur;
+    sg = nsg;
+    have = has_next;
   }
   if (after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #ifdef MYD_TIMELINE
   if (tid == 0) atomicMax(&g_tl[1], gtimer());
 #endif
 }
+
+void keep_pool_memory();  // capi.cu
 
 namespace {
 
@@ -569,11 +701,11 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>()>
+template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>(), bool SKM = false>
 cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                        const double *B,
                        int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
-                       int after_main, cudaStream_t st) {
+                       int after_main, cudaStream_t st, const StreamK &sk = StreamK{}) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
   // once per (device, instantiation); racing first calls just set it twice.
@@ -583,7 +715,7 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     cudaError_t e =
-        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
@@ -600,8 +732,8 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK>, M, N, K, A, lda, B, ldb, C, ldc,
-                                     tiles_m, tiles_n, tile0, edge, (int)units, after_main, ep);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM>, M, N, K, A, lda, B, ldb, C, ldc,
+                                     tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -625,6 +757,46 @@ cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, i
       return launch_one<VEC, 16, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
     default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
   }
+}
+
+// Full-tile slab depth, as launch_split's case 1 picks it.
+template <int VEC>
+constexpr int full_bk(int K) {
+  return (VEC == 2 && K >= 1024) ? 32 : 16;
+}
+
+inline void keep_pool_memory_fast() { keep_pool_memory(); }
+
+// Stream-K launch of the full-tile kernel over every SM (see the kernel's
+// segment comment): workspace of one partial tile per CTA plus per-warp flags
+// from the stream-ordered pool; the epoch makes stale flags never match.
+template <int VEC>
+cudaError_t launch_streamk(const Epilogue &ep, int M, int N, int K, const double *A, int64_t lda, const double *B,
+                           int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, long long tile0,
+                           int after_main, cudaStream_t st) {
+  static std::atomic<unsigned long long> epochs{0};
+  const int G = sm_count();
+  const int KT = (K + full_bk<VEC>(K) - 1) / full_bk<VEC>(K);
+  StreamK sk;
+  sk.dp_tiles = 0;
+  sk.tile0 = tile0;
+  sk.iters = ((long long)tiles_m * tiles_n - tile0) * KT;
+  sk.epoch = 0x5DA7000000000000ull | (epochs.fetch_add(1) + 1);
+  const size_t part = (size_t)G * fast::CONSUMER_WARPS * 32 * 64 * 8, flags = (size_t)G * fast::CONSUMER_WARPS * 8;
+  keep_pool_memory_fast();
+  void *ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, part + flags, st);
+  if (e != cudaSuccess) return e;
+  sk.work = static_cast<double *>(ws);
+  sk.flags = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + part);
+  if (full_bk<VEC>(K) == 32)
+    e = launch_one<VEC, 128, 128, 32, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                            after_main, st, sk);
+  else
+    e = launch_one<VEC, 128, 128, 16, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                            after_main, st, sk);
+  cudaFreeAsync(ws, st);
+  return e;
 }
 
 std::atomic<int> g_max_ctas{0};  // my_dgemm_set_max_ctas: 0 = every SM
@@ -681,7 +853,10 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   long long q = tiles / G;  // full-tile rounds of the main launch
   int split = 1;            // 1 full tiles; 2 / 4 / 8 units 128x64 / 128x32 / 64x32; 16 units 16x128
   auto per_tile = [](int s) { return s == 16 ? 8 : s; };
-  if (force_split > 1) {
+  bool streamk = force_split == 32 && tiles >= G;
+  if (force_split == 32) {
+    q = tiles;  // (no stream-K below one wave: full tiles instead)
+  } else if (force_split > 1) {
     split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
     q = 0;
   } else if (force_split == 0) {
@@ -735,6 +910,24 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         }
       }
     }
+    // Stream-K: the T*KT (tile, slab) iterations evenly over the SMs, a tile
+    // cut between two CTAs finished from the partial the first one leaves
+    // (bitwise the uncut chain).  Needs T >= G (a tile is cut at most once).
+    // Data-parallel rounds for all but the last (one to two waves of tiles).
+    if (tiles >= G && tiles % G != 0 && (G + tiles % G) * (long long)(K / 16 + 1) < (1LL << 30)) {
+      const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
+      const long long KT = (K + bk - 1) / bk, sk_tiles = G + tiles % G;
+      // the stream-K phase runs ~2 % slower per slab than whole tiles, and
+      // its launch, a PDL tail of the whole-tile rounds, costs ~5 us
+      // (tools/perf_probe.py --strips=32, profiles/plan_probe_sk_r01.log)
+      const double slab_us = 1.02 * (unit_us(1) - 2.8) / (double)KT;
+      const double cost = (double)(tiles / G - 1) * unit_us(1) + (tiles >= 2 * G ? 5.0 : 0.0) +
+                          (double)((sk_tiles * KT + G - 1) / G) * slab_us + 3 * 2.8 + 2.0;
+      if (cost < best - 1e-9) {
+        best = cost;
+        streamk = true;
+      }
+    }
     const int rem_m = M % TILE_M;
     if (rem_m >= 1 && rem_m <= 64) {  // ragged last tile row (or a problem < 64 rows) out of the raster
       const long long te = (long long)(tiles_m - 1) * tiles_n;
@@ -751,9 +944,24 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
           raster_n = tiles_n;
           edge = -ms;
           q = qe;
+          streamk = false;
         }
       }
     }
+  }
+  if (streamk) {
+    // whole-tile rounds for all but the last one-to-two waves in the unit-mode
+    // kernel, then the stream-K phase as a tail launch (its own tiles only)
+    const long long dp_tiles = (tiles / G - 1) * G;
+    cudaError_t e = cudaSuccess;
+    if (dp_tiles > 0)
+      e = vec2 ? launch_split<2>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
+                                 stream)
+               : launch_split<1>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
+                                 stream);
+    if (e != cudaSuccess) return e;
+    return vec2 ? launch_streamk<2>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles, dp_tiles > 0, stream)
+                : launch_streamk<1>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles, dp_tiles > 0, stream);
   }
   const long long raster_tiles = (long long)raster_m * raster_n;
   const long long main_tiles = split == 1 ? tiles : q * G;

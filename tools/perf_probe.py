@@ -26,9 +26,11 @@ def probe(m, n, k, reps=5, **kw):
     print(f"{m}x{n}x{k} {kw}: best {best:.3f} ms  {tf:.2f} TFLOP/s  ({tf/37.22*100:.1f}% of 37.22)", flush=True)
 
 quick = "--quick" in sys.argv
+strips = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--strips=")] or [0]
 sizes = [int(x) for x in sys.argv[1:] if not x.startswith("--")] or ([4096, 8192] if quick else [1024, 2048, 4096, 8192])
 for s in sizes:
-    probe(s, s, s)
+    for st_ in strips:
+        probe(s, s, s, **({"strips": st_} if st_ else {}))
 probe(16384, 16384, 256)
 probe(4093, 4099, 2047)
 if not quick:
