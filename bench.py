@@ -373,7 +373,7 @@ def run_b200_arm(args):
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                         "traffic": traffic, "kernel": "dgemm_fast_kernel<2,128> (+ <2,32> tail strips; one call = both launches)",
+                         "traffic": traffic, "kernel": "dgemm_fast_kernel<2,128,128,32> whole-tile rounds + stream-K tail (one call = both launches)",
                          "peak_source": "nominal FP64 148SMx128flop/clkx1.965GHz (not in MEASURED_PEAKS.json); "
                                         f"DMMA microbench {FP64_PEAK_MEASURED}",
                          "launches_timed": len(kern_ms), "mean_launch_ms": round(mean_kernel_s * 1e3, 4)},
