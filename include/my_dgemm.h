@@ -48,7 +48,8 @@ extern "C" {
 #define MY_DGEMM_FORCE_STRIPS4 0x20u /* run every tile as four 128x32 strips (tests) */
 #define MY_DGEMM_FORCE_UNITS8 0x40u  /* run every tile as eight 64x32 units (tests) */
 #define MY_DGEMM_FORCE_ROWS16 0x80u  /* run every tile as eight 16x128 units (tests) */
-#define MY_DGEMM_FORCE_STREAMK 0x800u /* stream-K schedule of full tiles when >= one wave (tests) */
+#define MY_DGEMM_FORCE_STREAMK 0x800u /* stream-K schedule (tests): of full tiles, or with STRIPS2 / STRIPS4 /
+                                          UNITS8 of those units, when there is at least one per SM */
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The

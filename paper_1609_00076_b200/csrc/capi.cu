@@ -105,12 +105,12 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     case MY_DGEMM_PATH_FEW_COLS: return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
     default: break;
   }
-  int split = (flags & MY_DGEMM_FORCE_STREAMK)   ? 32
-              : (flags & MY_DGEMM_FORCE_ROWS16)  ? 16
+  int split = (flags & MY_DGEMM_FORCE_ROWS16)    ? 16
               : (flags & MY_DGEMM_FORCE_UNITS8)  ? 8
               : (flags & MY_DGEMM_FORCE_STRIPS4) ? 4
               : (flags & MY_DGEMM_FORCE_STRIPS2) ? 2
                                                  : 0;
+  if (flags & MY_DGEMM_FORCE_STREAMK) split = 32 + (split == 16 ? 0 : split);  // stream-K over those units
   if (split == 0) split = tuned_plan(m, n, k, lda, ldb);  // 0 unless my_dgemm_tune chose one
   const bool force_vec1 = (flags & MY_DGEMM_FORCE_VEC1) != 0;
   const bool a_ok = lda % 2 == 0 && (uintptr_t)A % 16 == 0, b_ok = ldb % 2 == 0 && (uintptr_t)B % 16 == 0;

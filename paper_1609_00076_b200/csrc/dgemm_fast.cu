@@ -767,36 +767,77 @@ constexpr int full_bk(int K) {
 
 inline void keep_pool_memory_fast() { keep_pool_memory(); }
 
-// Stream-K launch of the full-tile kernel over every SM (see the kernel's
-// segment comment): workspace of one partial tile per CTA plus per-warp flags
-// from the stream-ordered pool; the epoch makes stale flags never match.
-template <int VEC>
-cudaError_t launch_streamk(const Epilogue &ep, int M, int N, int K, const double *A, int64_t lda, const double *B,
-                           int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, long long tile0,
-                           int after_main, cudaStream_t st) {
-  static std::atomic<unsigned long long> epochs{0};
-  const int G = sm_count();
-  const int KT = (K + full_bk<VEC>(K) - 1) / full_bk<VEC>(K);
+// Stream-K launch over every SM (see the kernel's segment comment) of the
+// BM x BN units from unit0 on (unit numbering of the unit-mode kernel with
+// tile0 = 0): workspace of one partial unit per CTA plus per-warp flags from
+// the stream-ordered pool; the epoch makes stale flags never match.
+// One epoch counter for every stream-K launch of the process (all
+// instantiations); the flags are also zeroed before every stream-K call, so
+// neither an earlier launch's flags nor other data left in pool memory can
+// match.
+std::atomic<unsigned long long> g_sk_epochs{0};
+
+// Workspace of one stream-K call: one partial unit per CTA plus per-warp
+// flags, from the stream-ordered pool, flags zeroed (before the call's first
+// launch, so the stream-K launch still follows its predecessor by PDL).
+struct SkWorkspace {
+  void *base = nullptr;
   StreamK sk;
+  cudaError_t alloc(int G, cudaStream_t st) {
+    const size_t part = (size_t)G * fast::CONSUMER_WARPS * 32 * 64 * 8, flags = (size_t)G * fast::CONSUMER_WARPS * 8;
+    keep_pool_memory_fast();
+    cudaError_t e = cudaMallocAsync(&base, part + flags, st);
+    if (e != cudaSuccess) return e;
+    sk.work = static_cast<double *>(base);
+    sk.flags = reinterpret_cast<unsigned long long *>(static_cast<char *>(base) + part);
+    sk.epoch = 0x5DA7000000000000ull | (g_sk_epochs.fetch_add(1) + 1);
+    return cudaMemsetAsync(sk.flags, 0, flags, st);
+  }
+  void release(cudaStream_t st) {
+    if (base) cudaFreeAsync(base, st);
+    base = nullptr;
+  }
+};
+
+// Stream-K launch over every SM (see the kernel's segment comment) of the
+// BM x BN units from unit0 on (unit numbering of the unit-mode kernel with
+// tile0 = 0).
+template <int VEC, int BM, int BN, int BK>
+cudaError_t launch_streamk(const Epilogue &ep, int M, int N, int K, const double *A, int64_t lda, const double *B,
+                           int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, long long unit0,
+                           int after_main, cudaStream_t st, StreamK sk) {
+  constexpr int PER_TILE = (fast::TILE_M / BM) * (fast::TILE_N / BN);
+  const int G = sm_count();
+  const int KT = (K + BK - 1) / BK;
   sk.dp_tiles = 0;
-  sk.tile0 = tile0;
-  sk.iters = ((long long)tiles_m * tiles_n - tile0) * KT;
-  sk.epoch = 0x5DA7000000000000ull | (epochs.fetch_add(1) + 1);
-  const size_t part = (size_t)G * fast::CONSUMER_WARPS * 32 * 64 * 8, flags = (size_t)G * fast::CONSUMER_WARPS * 8;
-  keep_pool_memory_fast();
-  void *ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, part + flags, st);
-  if (e != cudaSuccess) return e;
-  sk.work = static_cast<double *>(ws);
-  sk.flags = reinterpret_cast<unsigned long long *>(static_cast<char *>(ws) + part);
-  if (full_bk<VEC>(K) == 32)
-    e = launch_one<VEC, 128, 128, 32, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
-                                            after_main, st, sk);
-  else
-    e = launch_one<VEC, 128, 128, 16, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
-                                            after_main, st, sk);
-  cudaFreeAsync(ws, st);
-  return e;
+  sk.tile0 = unit0;
+  sk.iters = ((long long)tiles_m * tiles_n * PER_TILE - unit0) * KT;
+  return launch_one<VEC, BM, BN, BK, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                           after_main, st, sk);
+}
+
+// stream-K over units of `split` per tile (1 = full tiles), from unit0 on
+template <int VEC>
+cudaError_t launch_streamk_split(const Epilogue &ep, int split, int M, int N, int K, const double *A, int64_t lda,
+                                 const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n,
+                                 long long unit0, int after_main, cudaStream_t st, const StreamK &sk) {
+  switch (split) {
+    case 1:
+      if (full_bk<VEC>(K) == 32)
+        return launch_streamk<VEC, 128, 128, 32>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, unit0,
+                                                 after_main, st, sk);
+      return launch_streamk<VEC, 128, 128, 16>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, unit0,
+                                               after_main, st, sk);
+    case 2:
+      return launch_streamk<VEC, 128, 64, fast::default_bk<128, 64>()>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
+                                                                       tiles_n, unit0, after_main, st, sk);
+    case 4:
+      return launch_streamk<VEC, 128, 32, fast::default_bk<128, 32>()>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
+                                                                       tiles_n, unit0, after_main, st, sk);
+    default:
+      return launch_streamk<VEC, 64, 32, fast::default_bk<64, 32>()>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
+                                                                     tiles_n, unit0, after_main, st, sk);
+  }
 }
 
 std::atomic<int> g_max_ctas{0};  // my_dgemm_set_max_ctas: 0 = every SM
@@ -853,9 +894,10 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   long long q = tiles / G;  // full-tile rounds of the main launch
   int split = 1;            // 1 full tiles; 2 / 4 / 8 units 128x64 / 128x32 / 64x32; 16 units 16x128
   auto per_tile = [](int s) { return s == 16 ? 8 : s; };
-  bool streamk = force_split == 32 && tiles >= G;
-  if (force_split == 32) {
-    q = tiles;  // (no stream-K below one wave: full tiles instead)
+  int sk_split = force_split >= 32 ? (force_split == 32 ? 1 : force_split - 32) : 1;  // stream-K unit shape
+  bool streamk = force_split >= 32 && tiles * sk_split >= G;
+  if (force_split >= 32) {
+    q = tiles;  // (fewer units than SMs: plain full tiles instead)
   } else if (force_split > 1) {
     split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
     q = 0;
@@ -913,6 +955,23 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // Stream-K: the T*KT (tile, slab) iterations evenly over the SMs, a tile
     // cut between two CTAs finished from the partial the first one leaves
     // (bitwise the uncut chain).  Needs T >= G (a tile is cut at most once).
+    // Below one wave of tiles: stream-K over units (>= one unit per CTA, so a
+    // unit is cut at most once), when the problem has no ragged edge (empty
+    // units would be scheduled, not skipped).
+    if (tiles < G && M % TILE_M == 0 && N % TILE_N == 0)
+      for (int s : {2, 4, 8}) {
+        const long long units_s = tiles * s;
+        const int bk = s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : default_bk<64, 32>());
+        const long long KT = (K + bk - 1) / bk;
+        if (units_s < G || units_s * KT >= (1LL << 30)) continue;
+        const double slab_us = 1.02 * (unit_us(s) - (s == 2 ? 7.2 : (s == 4 ? 4.4 : 2.0))) / (double)KT;
+        const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + 3 * (s == 2 ? 7.2 : (s == 4 ? 4.4 : 2.0)) + 2.0;
+        if (cost < best - 1e-9) {
+          best = cost;
+          streamk = true;
+          sk_split = s;
+        }
+      }
     // Data-parallel rounds for all but the last (one to two waves of tiles).
     if (tiles >= G && tiles % G != 0 && (G + tiles % G) * (long long)(K / 16 + 1) < (1LL << 30)) {
       const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
@@ -926,6 +985,7 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       if (cost < best - 1e-9) {
         best = cost;
         streamk = true;
+        sk_split = 1;
       }
     }
     const int rem_m = M % TILE_M;
@@ -950,18 +1010,35 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     }
   }
   if (streamk) {
+    SkWorkspace ws;
+    cudaError_t e = ws.alloc((int)G, stream);
+    if (e != cudaSuccess) {
+      ws.release(stream);
+      return e;
+    }
+    if (sk_split > 1) {
+      e = vec2 ? launch_streamk_split<2>(ep, sk_split, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, stream,
+                                         ws.sk)
+               : launch_streamk_split<1>(ep, sk_split, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, stream,
+                                         ws.sk);
+      ws.release(stream);
+      return e;
+    }
     // whole-tile rounds for all but the last one-to-two waves in the unit-mode
     // kernel, then the stream-K phase as a tail launch (its own tiles only)
     const long long dp_tiles = (tiles / G - 1) * G;
-    cudaError_t e = cudaSuccess;
     if (dp_tiles > 0)
       e = vec2 ? launch_split<2>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
                                  stream)
                : launch_split<1>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
                                  stream);
-    if (e != cudaSuccess) return e;
-    return vec2 ? launch_streamk<2>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles, dp_tiles > 0, stream)
-                : launch_streamk<1>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles, dp_tiles > 0, stream);
+    if (e == cudaSuccess)
+      e = vec2 ? launch_streamk_split<2>(ep, 1, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles,
+                                         dp_tiles > 0, stream, ws.sk)
+               : launch_streamk_split<1>(ep, 1, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles,
+                                         dp_tiles > 0, stream, ws.sk);
+    ws.release(stream);
+    return e;
   }
   const long long raster_tiles = (long long)raster_m * raster_n;
   const long long main_tiles = split == 1 ? tiles : q * G;

@@ -205,6 +205,8 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
     (2100, 777, 300, 2101, 301, 2103),      # ragged row (52 rows) and column, odd lds
     (2048, 2048, 2048, 2048, 2048, 2048),   # stream-K: 256 tiles x 64 slabs over 148 SMs
     (3001, 2999, 1111, 3003, 1113, 3002),   # stream-K with ragged tiles, ragged last slab, odd lds
+    (1024, 1024, 1024, 1024, 1024, 1024),   # below one wave: stream-K over 128x64 / 128x32 / 64x32 units
+    (768, 1280, 600, 770, 602, 768),
 ])
 def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     """Full tiles, 128x64 strips, 128x32 strips, 64x32 and 16x128 units, the
@@ -213,7 +215,7 @@ def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     sequence does not depend on the CTA shape or on who runs which slabs)."""
     a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
     outs = []
-    for strips in (0, 2, 4, 8, 16, 32):
+    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40):
         cc = c.clone()
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips)
         outs.append(cc)

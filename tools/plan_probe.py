@@ -17,7 +17,7 @@ for s in sizes:
     c = torch.rand(s * s, dtype=torch.float64, device="cuda")
     inner = max(1, int(2e10 / (2.0 * s ** 3)))
     res = {}
-    for strips in (0, 2, 4, 8, 32):
+    for strips in (0, 2, 4, 8, 32, 34, 36, 40):
         def go():
             for _ in range(inner):
                 engine.dgemm_device(s, s, s, a.data_ptr(), s, b.data_ptr(), s, c.data_ptr(), s, st, strips=strips)
