@@ -158,7 +158,8 @@ MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, in
  * later calls of the same shape and operand alignment in this process.
  * Plans are bitwise-equivalent: tuning changes speed, never results.
  * out_plan: 0 heuristic, 1 full tiles, 2/4/8 units per tile (128x64 / 128x32 /
- * 64x32), 16 for 16x128 units.
+ * 64x32), 16 for 16x128 units, 32 / 34 / 36 / 40 stream-K over full tiles /
+ * 128x64 / 128x32 / 64x32 units.
  */
 MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan, double *out_ms);
 MY_DGEMM_API void my_dgemm_tune_clear(void);

@@ -74,7 +74,7 @@ extern "C" int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int
     if ((e = launch_fill_random(B, k, n, ldb, 2, 0, st)) != cudaSuccess) break;
     if ((e = launch_fill_random(C, m, n, ldc, 3, 0, st)) != cudaSuccess) break;
     if ((e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess) break;
-    const int plans[] = {0, 1, 2, 4, 8, 16};
+    const int plans[] = {0, 1, 2, 4, 8, 16, 32, 34, 36, 40};
     for (int plan : plans) {
       const Epilogue ep{};
       if ((e = launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, false, plan, ep)) != cudaSuccess) break;
