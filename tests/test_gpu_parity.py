@@ -515,7 +515,7 @@ def test_tuner_changes_speed_never_results(torch_cuda):
     c1 = c.clone()
     run_dev(torch_cuda, m, n, k, a, m, b, k, c1, m)
     plan, ms = engine.tune(m, n, k)
-    assert plan in (0, 1, 2, 4, 8) and ms > 0
+    assert plan in (0, 1, 2, 4, 8, 16, 32, 34, 36, 40) and ms > 0
     c2 = c.clone()
     run_dev(torch_cuda, m, n, k, a, m, b, k, c2, m)
     assert torch_cuda.equal(c1, c2)
