@@ -89,7 +89,7 @@ def test_invalid_arguments_status_and_untouched_c(lib, m, n, k, lda, ldb, ldc, n
 def test_unknown_flags_rejected(lib):
     a = np.zeros(16)
     assert lib.my_dgemm_ex(4, 4, 4, a.ctypes.data, 4, a.ctypes.data, 4, a.ctypes.data, 4,
-                           0x800, None) == -10
+                           0x1000, None) == -10
 
 
 def test_python_boundary_raises_reference_valueerrors(lib):
