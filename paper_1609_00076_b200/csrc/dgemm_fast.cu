@@ -9,8 +9,11 @@
 //                         tile column or a small problem is re-cut into
 //                         128x64 / 128x32 / 64x32 units so every SM gets work,
 //                         the plan chosen by a measured cost model
-//                         (launch_dgemm_fast); launches overlap their
-//                         neighbours by programmatic dependent launch;
+//                         (launch_dgemm_fast); a partial last wave can run
+//                         as stream-K (slabs of cut tiles split between two
+//                         CTAs, the exact accumulator state handed over, so C
+//                         is unchanged); launches overlap their neighbours by
+//                         programmatic dependent launch;
 //   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs;
 //   pack_a / pack_b    -> producer warps stage each A and B slab (and, first,
 //                         the unit's C block) into a multi-stage shared-memory
@@ -28,8 +31,9 @@
 //
 // Per-element arithmetic (k grouped in fours from p = 0, one DMMA per group,
 // groups in ascending order, accumulator starting at C) does not depend on
-// the unit shape, the tile position, the K-slab depth or the launch plan, so
-// every plan and every k-chunking at multiples of 16 gives bitwise the same C.
+// the unit shape, the tile position, the K-slab depth, the launch plan or
+// which CTA runs which slabs, so every plan (stream-K included) and every
+// k-chunking at multiples of 16 gives bitwise the same C.
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
