@@ -594,12 +594,13 @@ def test_device_flag_rejects_host_pointers(torch_cuda):
     assert st == -8
 
 
-def test_cuda_graph_capture_and_replay(torch_cuda):
+@pytest.mark.parametrize("m,n,k", [(300, 257, 129), (2048, 2048, 512), (1280, 1280, 300)])
+def test_cuda_graph_capture_and_replay(torch_cuda, m, n, k):
     """The device path is capture-safe: a CUDA graph of several my_dgemm_ex
-    calls replays to the same result as eager calls (launch-bound small
-    problems can be replayed without per-call host overhead)."""
+    calls replays, twice, to the same result as eager calls -- small units,
+    the stream-K schedule (workspace, zeroed flags and epoch baked into the
+    graph) and stream-K over units."""
     torch = torch_cuda
-    m, n, k = 300, 257, 129
     a, b, c, _ = dev_operands(torch, m, n, k)
     eager = c.clone()
     for _ in range(3):
@@ -615,6 +616,10 @@ def test_cuda_graph_capture_and_replay(torch_cuda):
             engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, graphed.data_ptr(), m,
                                 torch.cuda.current_stream().cuda_stream)
     g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(graphed, eager)
+    graphed.copy_(c)
+    g.replay()  # the flags of the previous replay must not satisfy this one's waits
     torch.cuda.synchronize()
     assert torch.equal(graphed, eager)
 
