@@ -422,8 +422,17 @@ cudaError_t launch_gemm_nsmall(int M, int N, int K, const double *A, int64_t lda
                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
   if (N <= 2) return launch_nsmall_t<2, 4, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
   if (N <= 4) return launch_nsmall_t<4, 4, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+#ifndef MYD_NS16_ROWS
+#define MYD_NS16_ROWS 2
+#endif
+#ifndef MYD_NS16_WARPS
+#define MYD_NS16_WARPS 4
+#endif
+#ifndef MYD_NS16_KW
+#define MYD_NS16_KW 8
+#endif
   if (N <= 8) return launch_nsmall_t<8, 2, 8, 8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
-  return launch_nsmall_t<16, 2, 8, 4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_nsmall_t<16, MYD_NS16_ROWS, MYD_NS16_WARPS, MYD_NS16_KW>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
 }
 
 namespace {
