@@ -815,3 +815,24 @@ def test_few_rows_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
     got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
     assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
+
+
+@pytest.mark.parametrize("m,n,k,alpha,beta", [(2048, 2048, 512, 1.5, -0.5), (2048, 2304, 700, 2.0, 0.0),
+                                               (1280, 1280, 300, -1.0, 1.0)])
+def test_blas_epilogue_under_stream_k(torch_cuda, m, n, k, alpha, beta):
+    """The BLAS epilogue (product from zero, alpha/beta at the end) through
+    the stream-K schedule: cut tiles carry the partial product, the last
+    segment applies alpha and beta once; beta = 0 never reads a NaN C."""
+    torch = torch_cuda
+    a, b, c, _ = dev_operands(torch, m, n, k)
+    cin = c.clone() if beta != 0 else torch.full_like(c, float("nan"))
+    out = cin.clone()
+    engine.dgemm("N", "N", m, n, k, alpha, a, m, b, k, beta, out, m)
+    torch.cuda.synchronize()
+    A = a.view(k, m).T
+    B = b.view(n, k).T
+    want = alpha * (A @ B) + (beta * c.view(n, m).T if beta != 0 else 0.0)
+    got = out.view(n, m).T
+    bound = HEADLINE_C * (k + 2) * EPS * (abs(alpha) * k + abs(beta))
+    assert torch.isfinite(got).all()
+    assert float((got - want).abs().max()) <= bound
