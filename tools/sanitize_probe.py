@@ -8,7 +8,8 @@ from paper_1609_00076_b200 import engine
 
 st = torch.cuda.current_stream().cuda_stream
 for (m, n, k, pa, pb, pc) in [(37, 53, 71, 7, 5, 3), (1, 70, 33, 7, 5, 3), (70, 1, 33, 7, 5, 3),
-                              (129, 130, 47, 1, 1, 1), (200, 260, 300, 0, 0, 0), (65, 33, 17, 2, 2, 2)]:
+                              (129, 130, 47, 1, 1, 1), (200, 260, 300, 0, 0, 0), (65, 33, 17, 2, 2, 2),
+                              (6, 300, 90, 1, 2, 3), (4100, 7, 60, 2, 1, 1), (1300, 1500, 100, 2, 2, 2)]:
     lda, ldb, ldc = m + pa, k + pb, m + pc
     a, b, c = oracle.make_padded_operands(42, m, n, k, lda, ldb, ldc)
     want = oracle.naive(m, n, k, a, lda, b, ldb, c.copy(), ldc)
@@ -16,7 +17,7 @@ for (m, n, k, pa, pb, pc) in [(37, 53, 71, 7, 5, 3), (1, 70, 33, 7, 5, 3), (70, 
         got = engine.my_dgemm(m, n, k, a, lda, b, ldb, c.copy(), ldc, **kw)
         assert np.abs(got - want).max() <= oracle.tolerance(k, 1, 1), (m, n, k, kw)
     # device path, exact-size buffers (no slack past (n-1)*ld+m), every unit shape
-    for strips in (0, 2, 4, 8):
+    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40):
         da = torch.from_numpy(a[: (k - 1) * lda + m].copy()).cuda()
         db = torch.from_numpy(b[: (n - 1) * ldb + k].copy()).cuda()
         dc = torch.from_numpy(c[: (n - 1) * ldc + m].copy()).cuda()
