@@ -236,10 +236,12 @@ def my_dgemm_multi(devices, m: int, n: int, k: int, A: np.ndarray, lda: int, B: 
 def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int, ldc: int,
                  stream: int = 0, exact: bool = False, force_tiled: bool = False,
                  force_vec1: bool = False, strips: int = 0, path: int | None = None) -> None:
-    """Raw device-pointer call (asynchronous on `stream`).  `strips` (2 or 4)
-    forces every tile through the narrow-strip kernels, 8 / 16 through the
-    64x32 / 16x128 units (tests); `path` forces a kernel family
-    (_capi.PATH_*, what sharded drivers pass to every shard)."""
+    """Raw device-pointer call (asynchronous on `stream`).  `strips` pins
+    the launch plan (tests, tuning): 2 / 4 / 8 / 16 every tile as 128x64 /
+    128x32 / 64x32 / 16x128 units, 32 / 34 / 36 / 40 the stream-K schedule
+    over full tiles / those units; `path` forces a kernel family
+    (_capi.PATH_*, what sharded drivers pass to every shard).  Every plan
+    gives bitwise the same C."""
     lib = _capi.load()
     _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
                                 _flags(exact, force_tiled, force_vec1, strips, path) | _capi.DEVICE_PTRS,
