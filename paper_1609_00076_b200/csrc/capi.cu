@@ -65,8 +65,8 @@ void keep_pool_memory() {
 
 // Which kernel a call uses (my_dgemm_path): the bandwidth kernels take the
 // shapes with one short dimension -- m == 1; few rows (m <= 4 with
-// n <= 16384, m <= 8 with n <= 4096: beyond that the tiled kernel's 16x128
-// units win); n == 1; few columns (n <= 16 with m >= 4096) -- every other
+// n <= 65536, m <= 8 with n <= 4096: beyond that the tiled kernel's 16x128
+// units win, tools/fewrows_vs_tiled.py); n == 1; few columns (n <= 16 with m >= 4096) -- every other
 // shape is tiled.  Sharded drivers pass the whole problem's path to every
 // shard (MY_DGEMM_FORCE_PATH), so a narrow shard never changes kernel.
 // Measurements: tools/nsmall_probe.py, tools/msmall_probe.py.
@@ -75,7 +75,7 @@ int path_kind(int m, int n, unsigned flags) {
   if (flags & MY_DGEMM_PATH_MASK) return (int)((flags & MY_DGEMM_PATH_MASK) >> 8) - 1;
   if (flags & MY_DGEMM_FORCE_TILED) return MY_DGEMM_PATH_TILED;
   if (m == 1) return MY_DGEMM_PATH_GEMV_M1;
-  if ((m <= 4 && n <= 16384) || (m <= 8 && n <= 4096)) return MY_DGEMM_PATH_FEW_ROWS;
+  if ((m <= 4 && n <= 65536) || (m <= 8 && n <= 4096)) return MY_DGEMM_PATH_FEW_ROWS;
   if (n == 1) return MY_DGEMM_PATH_GEMV_N1;
   if (n <= 16 && m >= 4096) return MY_DGEMM_PATH_FEW_COLS;
   return MY_DGEMM_PATH_TILED;

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(32 * WARPS)
         live[c] = j < j_end;
         bc[c] = B + (live[c] ? j : 0) * ldb + kb;
       }
-      constexpr int UNROLL = 4;
+      constexpr int UNROLL = MC <= 4 ? 8 : 4;  // B loads in flight per column (tools/msmall_variants.sh)
       int p = lane;
       for (; p + 32 * (UNROLL - 1) < kc; p += 32 * UNROLL) {
         double bv[UNROLL][MAXC];
@@ -452,9 +452,9 @@ cudaError_t launch_msmall_t(int M, int N, int K, const double *A, int64_t lda, c
       attr_done.fetch_or(bit, std::memory_order_release);
     }
   }
-  // each warp holds MAXC columns at a time; at most ~4 CTAs per SM
+  // each warp holds MAXC columns at a time; 8 (4-warp) or 2 (16-warp) CTAs per SM at most
   const int64_t want = std::min<int64_t>((N + (int64_t)WARPS * MAXC - 1) / ((int64_t)WARPS * MAXC),
-                                         4LL * sm_count_skinny());
+                                         (long long)(WARPS <= 4 ? 8 : 2) * sm_count_skinny());
   gemm_msmall_kernel<MC, MAXC, WARPS, KC>
       <<<(unsigned)want, 32 * WARPS, smem, stream>>>(M, N, K, A, lda, B, ldb, C, ldc, ep);
   count_launch();
@@ -466,7 +466,9 @@ cudaError_t launch_msmall_t(int M, int N, int K, const double *A, int64_t lda, c
 template <int MC>
 cudaError_t launch_msmall_cols(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
-  constexpr int WARPS = 8, KC = MC >= 16 ? 512 : 1024;
+  // measured (tools/msmall_variants.sh): 4-warp CTAs, 8 per SM, for <= 4 rows;
+  // 16-warp CTAs, 2 per SM, for 5..8 rows
+  constexpr int WARPS = MC <= 4 ? 4 : 16, KC = MC >= 16 ? 512 : 1024;
   const int64_t per_warp = N / ((int64_t)WARPS * 2 * sm_count_skinny());
   if constexpr (32 / MC >= 8)
     if (per_warp >= 8) return launch_msmall_t<MC, 8, WARPS, KC>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);

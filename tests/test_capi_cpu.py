@@ -205,7 +205,7 @@ FP = [(p + 1) << 8 for p in range(6)]  # MY_DGEMM_FORCE_PATH(p)
 
 @pytest.mark.parametrize("m,n,flags,want", [
     (8192, 8192, 0, 0), (8192, 1, 0, 1), (1, 8192, 0, 2), (1, 1, 0, 2), (8192, 16, 0, 3), (4095, 16, 0, 0),
-    (8192, 17, 0, 0), (4, 16384, 0, 4), (4, 16385, 0, 0), (5, 4096, 0, 4), (8, 4097, 0, 0), (2, 3, 0, 4),
+    (8192, 17, 0, 0), (4, 65536, 0, 4), (4, 65537, 0, 0), (5, 4096, 0, 4), (8, 4097, 0, 0), (2, 3, 0, 4),
     (9, 8192, 0, 0), (8, 1, 0, 4), (100, 1, 0, 1),
     (8192, 1, 0x4, 0), (4, 4, 0x4, 0), (4, 4, 0x2, 5),
     (8192, 1, FP[0], 0), (100, 1, FP[1], 1), (1, 50, FP[2], 2), (9000, 12, FP[3], 3), (16, 99999, FP[4], 4),
