@@ -194,6 +194,60 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
         assert abs(float(host_c[j, i]) - s["values"][t]) <= bound
 
 
+def test_cfg5_full_exact_samples_and_8_way_shards(torch_cuda, golden):
+    """cfg5 (32768^3, 8.6 GB per operand): every element of the fast result
+    against the exact (bitwise-oracle) kernel, the reference's sampled
+    elements (bitwise for exact, within the headline bound for fast), and the
+    8-rank jc-sharded step (multi.ShardedDgemm, 2048-deep k-chunks as the
+    overlapped schedule runs them; ranks one after another, A resident)
+    bitwise equal to the single call."""
+    from paper_1609_00076_b200.multi import ShardedDgemm, make_shard_plan
+
+    torch = torch_cuda
+    free, _ = torch.cuda.mem_get_info()
+    if free < 48 * 2**30:
+        pytest.skip("needs ~44 GB of device memory")
+    s = golden["sampled"]["cfg5"]
+    m, n, k = s["m"], s["n"], s["k"]
+    a, b, c, _ = dev_operands(torch, m, n, k)
+    fast = c.clone()
+    run_dev(torch, m, n, k, a, m, b, k, fast, m)
+    bound = HEADLINE_C * k * EPS * (k + 1)  # |A||B|+|C| <= k + 1 for entries in [-1, 1)
+    rows, cols = torch.tensor(s["rows"], device="cuda"), torch.tensor(s["cols"], device="cuda")
+    pick = lambda x: x.view(n, m)[cols][:, rows].T.reshape(-1).cpu().tolist()  # row-major over (rows, cols)
+    want = s["values"]
+    got_fast = pick(fast)
+    assert all(abs(g - w) <= bound for g, w in zip(got_fast, want))
+    plan = make_shard_plan(m, n, k, 8, root=0, k_chunk=2048)
+    shard = c.clone()
+    for rank in range(8):
+        j0, j1 = plan.local(rank)
+        drv = ShardedDgemm(plan, rank, broadcast=lambda t, src: None, overlap=True)
+        drv.step(a, m, b[j0 * k:], k, shard[j0 * m:], m, broadcast_a=False)
+    torch.cuda.synchronize()
+    assert torch.equal(shard, fast)
+    del shard
+    run_dev(torch, m, n, k, a, m, b, k, c, m, exact=True)  # c := the exact result
+    assert pick(c) == want  # bitwise the reference's elements
+    mx, i, j = engine.max_abs_diff_device(m, n, fast.data_ptr(), m, c.data_ptr(), m, bound)
+    assert i is None, (i, j, mx)
+
+
+def test_cfg4_full_fast_vs_exact(torch_cuda, golden):
+    """cfg4 (16384^2 x 256, the rank-k panel): fast against exact on every
+    element; the exact result is the reference KAT bit for bit."""
+    kat = golden["kat"]["cfg4"]
+    m, n, k = kat["m"], kat["n"], kat["k"]
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    ce = c.clone()
+    run_dev(torch_cuda, m, n, k, a, m, b, k, c, m)
+    run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
+    assert oracle.sha256_valid(ce.cpu().numpy(), m, n, m) == kat["sha256"]
+    bound = HEADLINE_C * k * EPS * (k + 1)
+    mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), m, ce.data_ptr(), m, bound)
+    assert i is None, (i, j, mx)
+
+
 @pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
     (1000, 1100, 300, 1000, 300, 1000),     # aligned: bulk-copy path
     (777, 1029, 201, 781, 205, 780),        # odd ld: 8-byte LDGSTS path
