@@ -306,6 +306,12 @@ def run_b200_arm(args):
         launch_events.append((e0, e1, kc))
 
     drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=args.overlap, reserve_sms=args.reserve_sms)
+    close_chain = None
+    if world > 1 and args.exchange == "chain":  # A over NVLink by the copy engines (peer.py)
+        from paper_1609_00076_b200.peer import connect_chain
+
+        chain, close_chain = connect_chain(A, drv.chain_spans(m), rank, world, root=0)
+        drv.attach_chain(chain)
 
     def step():
         drv.step(A, m, B, k, C, m)
@@ -348,6 +354,10 @@ def run_b200_arm(args):
     flop_step = 2.0 * m * n_total * k
     value = flop_step * args.steps / (ms_max * 1e-3) / 1e9
 
+    exchange_name = ("copy-engine chain over NVLink peer memory" if args.exchange == "chain"
+                     else "NCCL broadcast")
+    if close_chain is not None:
+        close_chain()
     e2e = None
     if not args.no_e2e:
         e2e = measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total)
@@ -368,8 +378,8 @@ def run_b200_arm(args):
             "config": {"workload": args.workload, "m": m, "n": n_total, "k": k,
                        "n_per_gpu": nloc, "lda": m, "ldb": k, "ldc": m, "layout": "column-major",
                        "parallelism": f"jc-shard x{world}" + (
-                           (f", NCCL broadcast of A in {len(plan.chunks)} k-chunks under the GEMM" if args.overlap
-                            else ", NCCL broadcast of A, then the GEMM") if world > 1 else ""),
+                           (f", {exchange_name} of A in {len(drv.plan.chunks)} k-chunks under the GEMM" if args.overlap
+                            else f", {exchange_name} of A, then the GEMM") if world > 1 else ""),
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
@@ -469,6 +479,9 @@ def main():
                          "--workload cfg5 --strong: SURVEY 8e's 32768^3 on 1/2/4/8 GPUs)")
     ap.add_argument("--overlap", action="store_true",
                     help="broadcast A in k-chunks under the GEMM instead of before it (N>1)")
+    ap.add_argument("--exchange", choices=("nccl", "chain"), default="nccl",
+                    help="N > 1: how A reaches the ranks -- NCCL broadcast, or the copy-engine chain over "
+                         "NVLink peer memory (no SMs; paper_1609_00076_b200/peer.py)")
     ap.add_argument("--reserve-sms", type=int, default=0,
                     help="with --overlap: SMs kept free of the GEMM for NCCL's kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")

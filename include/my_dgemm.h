@@ -190,6 +190,32 @@ MY_DGEMM_API int my_dgemm_set_max_ctas(int n);
 #define MY_DGEMM_PATH_EXACT 5    /* MY_DGEMM_EXACT */
 MY_DGEMM_API int my_dgemm_path(int m, int n, unsigned flags);
 
+/*
+ * NVLink peer-memory plumbing of the multi-GPU driver's exchange step (the A
+ * broadcast of SURVEY 8e; the reference's threads share A in one address
+ * space, pkg/src/gemmforge/parallel.py:108-243, so it has no counterpart
+ * call).  paper_1609_00076_b200/peer.py builds a copy-engine chain from them:
+ * each rank pulls k-chunks of A from its predecessor's HBM and signals its
+ * successor, all stream-ordered, no SM involved.
+ *
+ * my_dgemm_ipc_export: CUDA IPC handle (MY_DGEMM_IPC_HANDLE_BYTES bytes) of the
+ *   allocation holding dev_ptr, and dev_ptr's offset in it.
+ * my_dgemm_ipc_open / _close: map another process's buffer (lazy peer access);
+ *   returns base + offset.  Not within the exporting process.
+ * my_dgemm_signal_write: stream-ordered 32-bit store to a (local or peer-mapped)
+ *   device flag, after the stream's earlier work is complete and visible.
+ * my_dgemm_signal_wait_geq: the stream waits until (int32_t)(*flag - value) >= 0.
+ * my_dgemm_copy_async: stream-ordered copy between device (or peer) addresses
+ *   by the copy engines.
+ */
+#define MY_DGEMM_IPC_HANDLE_BYTES 64
+MY_DGEMM_API int my_dgemm_ipc_export(const void *dev_ptr, unsigned char *handle_out, uint64_t *offset_out);
+MY_DGEMM_API int my_dgemm_ipc_open(const unsigned char *handle, uint64_t offset, void **dev_ptr_out);
+MY_DGEMM_API int my_dgemm_ipc_close(void *dev_ptr, uint64_t offset);
+MY_DGEMM_API int my_dgemm_signal_write(void *stream, uint32_t *dev_flag, uint32_t value);
+MY_DGEMM_API int my_dgemm_signal_wait_geq(void *stream, const uint32_t *dev_flag, uint32_t value);
+MY_DGEMM_API int my_dgemm_copy_async(void *dst, const void *src, uint64_t bytes, void *stream);
+
 /* Diagnostics. */
 MY_DGEMM_API const char *my_dgemm_last_error(void);
 MY_DGEMM_API int my_dgemm_last_status(void);

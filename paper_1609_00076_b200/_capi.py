@@ -24,6 +24,7 @@ FORCE_STRIPS4 = 0x20
 FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
 FORCE_STREAMK = 0x800
+IPC_HANDLE_BYTES = 64
 PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT = range(6)
 
 
@@ -53,6 +54,12 @@ SIGNATURES = {
     "my_dgemm_tune_clear": (None, []),
     "my_dgemm_set_max_ctas": (_I, [_I]),
     "my_dgemm_path": (_I, [_I, _I, ctypes.c_uint]),
+    "my_dgemm_ipc_export": (_I, [_P, ctypes.c_char_p, ctypes.POINTER(_U64)]),
+    "my_dgemm_ipc_open": (_I, [ctypes.c_char_p, _U64, ctypes.POINTER(_P)]),
+    "my_dgemm_ipc_close": (_I, [_P, _U64]),
+    "my_dgemm_signal_write": (_I, [_P, _P, ctypes.c_uint32]),
+    "my_dgemm_signal_wait_geq": (_I, [_P, _P, ctypes.c_uint32]),
+    "my_dgemm_copy_async": (_I, [_P, _P, _U64, _P]),
     "my_dgemm_last_error": (ctypes.c_char_p, []),
     "my_dgemm_last_status": (_I, []),
     "my_dgemm_version": (ctypes.c_char_p, []),

@@ -18,7 +18,10 @@ depends only on A and column j of B.  So:
     ShardedDgemm);
   * each rank runs C_g += A[:, chunk] * B_g[chunk, :] in ascending chunk
     order (my_dgemm_shard), the reference's pc order, so C is bitwise
-    identical for every world size.
+    identical for every world size;
+  * instead of NCCL, A can travel down a copy-engine chain over NVLink peer
+    memory (attach_chain, peer.py): no SM is involved, so the transfer
+    overlaps the persistent GEMM without competing for SMs.
 
 The compute and broadcast callables are injectable so the host logic runs
 under gloo on CPU in tests (tests/test_multi.py); the product path uses the
@@ -103,8 +106,13 @@ class ShardedDgemm:
 
     def __init__(self, plan: ShardPlan, rank: int, group=None,
                  compute: Callable | None = None, broadcast: Callable | None = None,
-                 force_tiled: bool | None = None, overlap: bool = False, reserve_sms: int = 0):
+                 force_tiled: bool | None = None, overlap: bool = False, reserve_sms: int = 0,
+                 stream: Callable | None = None):
         self.plan, self.rank, self.group = plan, rank, group
+        # exchange of A: NCCL broadcast (default) or, once attach_chain() is
+        # called, the copy-engine chain over NVLink peer memory (peer.py)
+        self.chain = None
+        self._stream = stream or self._current_stream
         # overlap=True with reserve_sms > 0 caps the GEMM's persistent grid at
         # (SM count - reserve_sms) CTAs during the step (my_dgemm_set_max_ctas)
         # so the broadcast's NCCL kernels always find free SMs; C is unchanged.
@@ -134,6 +142,12 @@ class ShardedDgemm:
         self._broadcast = broadcast or self._nccl_broadcast
 
     # -- defaults (GPU) ---------------------------------------------------
+    @staticmethod
+    def _current_stream():
+        import torch
+
+        return torch.cuda.current_stream()
+
     def _device_compute(self, m, nloc, kc, A, lda, B, ldb, C, ldc):
         import torch
 
@@ -147,11 +161,42 @@ class ShardedDgemm:
 
         return dist.broadcast(tensor, src=src, group=self.group, async_op=True)
 
+    # -- copy-engine chain ------------------------------------------------
+    def chain_spans(self, lda: int) -> tuple[tuple[int, int], ...]:
+        """A's element span of every k-chunk of this driver's plan: the
+        spans a PeerChain for it must be built with."""
+        return tuple(a_span(lda, self.plan.m, p0, p1) for (p0, p1) in self.plan.chunks)
+
+    def attach_chain(self, chain) -> None:
+        """Exchange A through `chain` (peer.PeerChain over chain_spans())."""
+        self.chain = chain
+
+    def _step_chain(self, A, lda, B_local, ldb, C_local, ldc):
+        p = self.plan
+        nloc = p.local(self.rank)[1] - p.local(self.rank)[0]
+        cs = self._stream()
+        events = self.chain.issue(cs)
+        if self.overlap:  # chunk c's GEMM as soon as chunk c has landed
+            for ci, (p0, p1) in enumerate(p.chunks):
+                self.chain.wait_chunk(cs, events, ci)
+                if nloc > 0:
+                    lo, hi = a_span(lda, p.m, p0, p1)
+                    self._compute(p.m, nloc, p1 - p0, A[lo:hi], lda, B_local[p0:], ldb, C_local, ldc)
+        else:
+            for ci in range(len(p.chunks)):
+                self.chain.wait_chunk(cs, events, ci)
+            if nloc > 0:
+                self._compute(p.m, nloc, p.k, A[:a_span(lda, p.m, 0, p.k)[1]], lda, B_local, ldb, C_local, ldc)
+        self.chain.finish(cs)
+        return C_local
+
     # -- one step ---------------------------------------------------------
     def step(self, A, lda: int, B_local, ldb: int, C_local, ldc: int, broadcast_a: bool = True):
         p = self.plan
         j0, j1 = p.local(self.rank)
         nloc = j1 - j0
+        if self.chain is not None and p.world > 1 and broadcast_a:
+            return self._step_chain(A, lda, B_local, ldb, C_local, ldc)
         if not self.overlap:
             if p.world > 1 and broadcast_a:
                 lo, hi = a_span(lda, p.m, 0, p.k)
