@@ -79,6 +79,10 @@ __device__ unsigned long long g_fast_prof[8];
 #define PROF_ADD(i, v)
 #endif
 
+#ifndef MYD_EP_SHFL
+#define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
+#endif
+
 namespace fast {
 #ifndef MYD_FAST_SMEM_KB
 #define MYD_FAST_SMEM_KB 224
@@ -653,6 +657,35 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       const int col0 = sg.n0 + wn * WN + r;
       // ---- epilogue: valid region only (padding rows never touched) ----
       const bool vec_store = c_aligned;
+      bool stored = false;
+#if MYD_EP_SHFL
+      // Interior units: lanes r < 4 and r >= 4 (lane ^ 16) swap one pair of
+      // every two row-fragments so each warp store writes 4 columns x 128
+      // contiguous bytes instead of 8 columns x 64: half the cache lines per
+      // store instruction, which is what bounds the write-back of a unit.
+      if constexpr (FM % 2 == 0) {
+        if (!ep.blas && c_aligned && sg.m0 + BM <= M && sg.n0 + BN <= N) {
+          const bool lo = r < 4;
+          const int rowb = row0 + (lo ? 0 : 8), colb = col0 - (lo ? 0 : 4);
+#pragma unroll
+          for (int i = 0; i < FM; i += 2)
+#pragma unroll
+            for (int j = 0; j < FN; ++j) {
+              const double s0 = lo ? acc[i + 1][j][0] : acc[i][j][0];
+              const double s1 = lo ? acc[i + 1][j][1] : acc[i][j][1];
+              const double g0 = __shfl_xor_sync(0xffffffffu, s0, 16);
+              const double g1 = __shfl_xor_sync(0xffffffffu, s1, 16);
+              double *cp = C + (int64_t)(colb + j * 8) * ldc + rowb + i * 8;
+              *reinterpret_cast<double2 *>(cp) =
+                  lo ? make_double2(acc[i][j][0], acc[i][j][1]) : make_double2(g0, g1);
+              *reinterpret_cast<double2 *>(cp + 4 * ldc) =
+                  lo ? make_double2(g0, g1) : make_double2(acc[i + 1][j][0], acc[i + 1][j][1]);
+            }
+          stored = true;
+        }
+      }
+#endif
+      if (!stored)
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
