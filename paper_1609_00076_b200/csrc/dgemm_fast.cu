@@ -229,6 +229,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
+#ifdef MYD_TIMELINE
+  int unit_ord = 0;  // units finished by this consumer warp (timeline marks)
+  if (tid == 0 && !after_main) atomicMin(&g_tl[0], gtimer());
+#endif
   const int KT = (K + BK - 1) / BK;
 
   // Work segments.  Unit mode (sk.iters == 0): unit u, all K slabs, from C to
@@ -647,6 +651,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     const int ncur = seg_next(cur, sg);
     Seg nsg;
     const bool has_next = seg_at(ncur, nsg);
+    bool c_loaded = false;  // the next unit's C block already in the accumulators
     if (!sg.to_c) {
       store_partial(sg.slot);  // the lower slabs of a tile another CTA finishes
     } else {
@@ -667,6 +672,13 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         if (!ep.blas && c_aligned && sg.m0 + BM <= M && sg.n0 + BN <= N) {
           const bool lo = r < 4;
           const int rowb = row0 + (lo ? 0 : 8), colb = col0 - (lo ? 0 : 4);
+          // The next unit's C block (already staged in the ring) is read into
+          // each fragment pair right after that pair is stored, so the
+          // shared-memory reads overlap the global write-back.
+          const uint32_t gn = g + NS;
+          const bool pre = has_next && nsg.from_c;
+          if (pre)
+            for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(gn + cs) % STAGES], ((gn + cs) / STAGES) & 1);
 #pragma unroll
           for (int i = 0; i < FM; i += 2)
 #pragma unroll
@@ -680,7 +692,21 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
                   lo ? make_double2(acc[i][j][0], acc[i][j][1]) : make_double2(g0, g1);
               *reinterpret_cast<double2 *>(cp + 4 * ldc) =
                   lo ? make_double2(g0, g1) : make_double2(acc[i + 1][j][0], acc[i + 1][j][1]);
+              if (pre) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
+                  acc[i + h][j][0] = v.x;
+                  acc[i + h][j][1] = v.y;
+                }
+              }
             }
+          if (pre) {
+            __syncwarp();
+            if (lane == 0)
+              for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(gn + cs) % STAGES]);
+            c_loaded = true;
+          }
           stored = true;
         }
       }
@@ -708,7 +734,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         }
     }
     g += NS;
-    if (has_next) g = init_acc(nsg, g);
+    if (has_next) g = c_loaded ? g + CS : init_acc(nsg, g);
     TL_MARK(6);
 #ifdef MYD_TIMELINE
     ++unit_ord;
