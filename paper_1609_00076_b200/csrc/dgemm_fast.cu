@@ -965,15 +965,16 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
     q = 0;
   } else if (force_split == 0) {
-    auto unit_us = [&](int s) {  // one unit of 1/s tile, depth K, on one SM (fitted)
+    // one unit of 1/s tile, depth K, on one SM: ideal / e_s + b_s microseconds
+    // (fitted: tools/plan_probe.py, profiles/plan_probe_r01b.log; b_8 refitted
+    // on whole-call timings of 256-4096^3, tools/midsize_plans.py,
+    // profiles/midsize_plans_r01.log, where 4 us instead of 2 stops 64x32
+    // units winning at 768-1280^3 by a model margin they do not have)
+    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 2.0 : 4.0))); };
+    auto unit_us = [&](int s) {
       const double ideal = 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3;
-      switch (s) {
-        case 1: return ideal / 0.990 + 2.8;
-        case 2: return ideal / 0.984 + 7.2;
-        case 4: return ideal / 0.983 + 4.4;
-        case 16: return ideal / 0.970 + 2.0;
-        default: return ideal / 0.977 + 2.0;
-      }
+      const double e = s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : (s == 16 ? 0.970 : 0.977)));
+      return ideal / e + unit_b(s);
     };
     auto rounds = [&](long long units) { return (double)((units + G - 1) / G); };
     constexpr double SECOND_LAUNCH_US = 15.0;
@@ -1027,8 +1028,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         const int bk = s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : default_bk<64, 32>());
         const long long KT = (K + bk - 1) / bk;
         if (units_s < G || units_s * KT >= (1LL << 30)) continue;
-        const double slab_us = 1.02 * (unit_us(s) - (s == 2 ? 7.2 : (s == 4 ? 4.4 : 2.0))) / (double)KT;
-        const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + 3 * (s == 2 ? 7.2 : (s == 4 ? 4.4 : 2.0)) + 2.0;
+        // stream-K phase slabs run ~2 % slower than whole units (~15 % for 64x32 units)
+        const double slab_us = (s == 8 ? 1.15 : 1.02) * (unit_us(s) - unit_b(s)) / (double)KT;
+        const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + 3 * unit_b(s) + 2.0;
         if (cost < best - 1e-9) {
           best = cost;
           streamk = true;
@@ -1042,9 +1044,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       // the stream-K phase runs ~2 % slower per slab than whole tiles, and
       // its launch, a PDL tail of the whole-tile rounds, costs ~5 us
       // (tools/perf_probe.py --strips=32, profiles/plan_probe_sk_r01.log)
-      const double slab_us = 1.02 * (unit_us(1) - 2.8) / (double)KT;
+      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)KT;
       const double cost = (double)(tiles / G - 1) * unit_us(1) + (tiles >= 2 * G ? 5.0 : 0.0) +
-                          (double)((sk_tiles * KT + G - 1) / G) * slab_us + 3 * 2.8 + 2.0;
+                          (double)((sk_tiles * KT + G - 1) / G) * slab_us + 3 * unit_b(1) + 2.0;
       if (cost < best - 1e-9) {
         best = cost;
         streamk = true;
