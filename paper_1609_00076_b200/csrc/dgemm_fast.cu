@@ -394,8 +394,14 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       }
       // Interior units with 16-byte aligned operands use the bulk-copy (TMA)
       // engine straight into the padded slab layout, with no LSU traffic.
-      // Edge units and a ragged last slab use zero-filling LDGSTS.
-      const bool interior = (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
+      // Edge units and a ragged last slab use zero-filling LDGSTS.  So do the
+      // 16x128 units: their slab is 160 small copies (32 A rows of 128 B, 128
+      // B columns of 256 B) per 1024 DMMA cycles, more than the bulk-copy
+      // engine issues -- LDGSTS staging runs them 1.8x faster, while every
+      // other shape is 3-5 % faster with bulk copies
+      // (profiles/rows16_staging_r01.log).
+      constexpr bool BULK_UNIT = BM != 16;
+      const bool interior = BULK_UNIT && (VEC == 2) && (m0 + BM <= M) && (n0 + BN <= N);
       for (int kt = sg.kb; kt < sg.ke; ++kt, ++g) {
         const int slot = g % STAGES;
         if (g >= STAGES) {
@@ -969,11 +975,12 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // (fitted: tools/plan_probe.py, profiles/plan_probe_r01b.log; b_8 refitted
     // on whole-call timings of 256-4096^3, tools/midsize_plans.py,
     // profiles/midsize_plans_r01.log, where 4 us instead of 2 stops 64x32
-    // units winning at 768-1280^3 by a model margin they do not have)
-    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 2.0 : 4.0))); };
+    // units winning at 768-1280^3 by a model margin they do not have; 16x128
+    // units, LDGSTS-staged, refitted on tools/rows16_probe.py: e 0.74, b 0.5)
+    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 0.5 : 4.0))); };
     auto unit_us = [&](int s) {
       const double ideal = 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3;
-      const double e = s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : (s == 16 ? 0.970 : 0.977)));
+      const double e = s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : (s == 16 ? 0.740 : 0.977)));
       return ideal / e + unit_b(s);
     };
     auto rounds = [&](long long units) { return (double)((units + G - 1) / G); };

@@ -8,7 +8,9 @@ def t(fn):
     for _ in range(10):
         e0,e1=torch.cuda.Event(enable_timing=True),torch.cuda.Event(enable_timing=True); e0.record(); fn(); e1.record(); torch.cuda.synchronize(); best=min(best,e0.elapsed_time(e1)*1e3)
     return best
-for m,n,k in [(8,8192,8192),(8,32768,8192),(4,100000,2000),(4,32768,8192),(6,8192,8192),(8,6000,4000),(5,50000,3000)]:
+SHAPES = [(m, n, 8192) for m in (2, 3, 4, 5, 6, 8) for n in (2048, 4096, 8192, 16384, 32768)] + \
+    [(4, 65536, 4096), (4, 131072, 2048), (2, 131072, 2048), (8, 65536, 2048), (6, 50000, 3000)]
+for m,n,k in SHAPES:
     a=torch.rand(m*k,dtype=torch.float64,device="cuda"); b=torch.rand(k*n,dtype=torch.float64,device="cuda"); c=torch.rand(m*n,dtype=torch.float64,device="cuda")
     r={}
     for p in (_capi.PATH_FEW_ROWS, _capi.PATH_TILED):
