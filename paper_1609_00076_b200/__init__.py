@@ -4,8 +4,9 @@ reference's `my_dgemm` path (BLISlab, arXiv:1609.00076; reference package
 
 The hot path is hand-written CUDA in csrc/ compiled to libmy_dgemm_b200.so,
 whose C ABI is include/my_dgemm.h.  This package is the host-side mirror of
-the reference's engine/registry interface (engine.py) and the jc-sharded
-multi-GPU driver (multi.py).  There is no CPU fallback: calls raise when the
+the reference's engine/registry interface (engine.py), the jc-sharded
+multi-GPU driver (multi.py) and its copy-engine exchange of A over NVLink
+peer memory (peer.py).  There is no CPU fallback: calls raise when the
 library is absent.
 """
 
