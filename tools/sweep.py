@@ -8,7 +8,8 @@ cfg5 32768^3 (1 GPU).  Operands come from the device generator (seed 42).
 Timing: CUDA events on the launch stream, 2 warm-ups, best and median of
 `reps`; C is reset from a pristine copy outside the timed region when the
 operands fit in L2-sized budgets, else left accumulating (same work).
-Reports GFLOP/s, fraction of 37.22 TF FP64 peak, and GB/s over the
+Reports GFLOP/s, fraction of 37.22 TF FP64 peak, the median SM clock and
+throttle reasons nvidia-smi saw while timing, and GB/s over the
 algorithmic bytes 8(mk + kn + 2mn) against the 6550.7 GB/s measured HBM copy.
 """
 
@@ -20,6 +21,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from bench import ClockSampler  # noqa: E402  (nvidia-smi sampling, as the bench line does)
 from paper_1609_00076_b200 import engine  # noqa: E402
 
 PEAK_TF = 37.22
@@ -49,6 +51,8 @@ def run(name, m, n, k, lda=None, ldb=None, ldc=None, reps=5):
         go()
     torch.cuda.synchronize()
     times = []
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
     for _ in range(reps):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -57,12 +61,14 @@ def run(name, m, n, k, lda=None, ldb=None, ldc=None, reps=5):
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3 / inner)
+    clk = clocks.stop()
     best, med = min(times), statistics.median(times)
     byts = 8.0 * (m * k + k * n + 2 * m * n)
     rec = {"config": name, "m": m, "n": n, "k": k, "lda": lda, "ldb": ldb, "ldc": ldc,
            "launches_per_event": inner, "best_us": round(best * 1e6, 2), "median_us": round(med * 1e6, 2),
            "gflops": round(flop / best / 1e9, 2), "frac_fp64_peak": round(flop / best / 1e12 / PEAK_TF, 4),
-           "gbs": round(byts / best / 1e9, 1), "frac_hbm": round(byts / best / 1e9 / HBM_GBS, 4)}
+           "gbs": round(byts / best / 1e9, 1), "frac_hbm": round(byts / best / 1e9 / HBM_GBS, 4),
+           "sm_mhz": clk.get("sm_mhz"), "clock_reasons": clk.get("reasons")}
     print(json.dumps(rec), flush=True)
     del a, b, c
     torch.cuda.empty_cache()
