@@ -15,11 +15,13 @@
 //                         is unchanged); launches overlap their neighbours by
 //                         programmatic dependent launch;
 //   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs;
-//   pack_a / pack_b    -> producer warps stage each A and B slab (and, first,
-//                         the unit's C block) into a multi-stage shared-memory
-//                         ring: bulk copies by the TMA engine (cp.async.bulk)
-//                         for aligned interior data, zero-filling cp.async
-//                         (LDGSTS) at the edges; no pack pass touches HBM;
+//   pack_a / pack_b    -> producer warps stage each A and B slab (and, for
+//                         narrow units, first the unit's C block; full tiles
+//                         read C from global, prefetched to L2) into a
+//                         multi-stage shared-memory ring: bulk copies by the
+//                         TMA engine (cp.async.bulk) for aligned interior
+//                         data, zero-filling cp.async (LDGSTS) at the edges
+//                         and for 16x128 units; no pack pass touches HBM;
 //   loops 2/1 + _mk    -> 8 consumer warps, each a register tile of C built
 //                         from DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
 //                         no tcgen05 kind on sm_100a; the DMMA pipe measured
@@ -79,6 +81,9 @@ __device__ unsigned long long g_fast_prof[8];
 #define PROF_ADD(i, v)
 #endif
 
+#ifndef MYD_CGLOBAL
+#define MYD_CGLOBAL 1  // full 128x128 tiles read C from global memory (0: through the ring, for A/B timing)
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -180,6 +185,16 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   constexpr int FM = WM / 8, FN = WN / 8;
   constexpr int RW = BN / PRODUCER_WARPS;  // B rows staged by each producer warp
   static_assert(WARPS_M * WARPS_N == CONSUMER_WARPS && FM >= 1 && RW >= 8, "tile shape");
+  // Full tiles of the unit-mode kernel read their C block straight from
+  // global memory (the producers prefetch it to L2 when they start the
+  // unit; the consumers read it into each fragment pair right after storing
+  // that pair of the previous unit) instead of staging it through ring slots:
+  // the C block no longer takes 2 of 3 (BK 32) or 4 of 6 (BK 16) slots at
+  // every unit boundary, so slab prefetch keeps going across it.  cfg4
+  // 91.4 -> 94.3 %, k = 128 85.5 -> 91.5 %, 8192^3 +0.2 %
+  // (profiles/c_from_global_r01.log).  Narrower units keep the ring path
+  // (measured slower this way); so does the stream-K kernel.
+  constexpr bool CG = MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && !SKM;
 
   extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
@@ -354,7 +369,15 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // the BLAS epilogue reads C at the end instead).  The copies are issued
       // while the consumers finish the previous unit, so the C load is off the
       // critical path and spread in time instead of bursting at unit start.
-      if (!ep.blas && sg.from_c) {
+      if (CG && !ep.blas && sg.from_c) {
+        const int rows = max(0, min(BM, M - m0));
+        const int col = pw * (BN / PRODUCER_WARPS) + lane;
+        if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PRODUCER_WARPS && n0 + col < N)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(C + (int64_t)(n0 + col) * ldc + m0),
+                       "r"(rows * 8)
+                       : "memory");
+      }
+      if (!CG && !ep.blas && sg.from_c) {
         const bool c_bulk = c_aligned && (m0 + BM <= M) && (n0 + BN <= N);
         for (int cs = 0; cs < CS; ++cs, ++g) {
           const int slot = g % STAGES;
@@ -584,6 +607,21 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         acc[i][j][1] = v.y;
       }
   };
+  // CG: fragment pair (i, j) of a unit at (row0, col0) straight from C
+  auto load_c_pair = [&](int i, int j, int row0, int col0, bool inside) {
+    const int row = row0 + i * 8, col = col0 + j * 8;
+    const double *cp = C + (int64_t)col * ldc + row;
+    if (inside) {
+      const double2 v = __ldcg(reinterpret_cast<const double2 *>(cp));
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    } else {
+      acc[i][j][0] = (row < M && col < N) ? __ldcg(cp) : 0.0;
+      acc[i][j][1] = (row + 1 < M && col < N) ? __ldcg(cp + 1) : 0.0;
+    }
+  };
+  auto c_inside = [&](const Seg &s) { return c_aligned && s.m0 + BM <= M && s.n0 + BN <= N; };
+  constexpr int CSR = CG ? 0 : CS;  // ring slots a unit's C block occupies
   // accumulator initialisation of a segment whose C block (if any) sits at
   // ring position gpos; returns the ring position of its first slab
   auto init_acc = [&](const Seg &sg, uint32_t gpos) -> uint32_t {
@@ -591,8 +629,18 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       load_partial(sg.slot);
       return gpos;
     }
+    if constexpr (CG) {
+      if (!ep.blas) {
+        const bool inside = c_inside(sg);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) load_c_pair(i, j, sg.m0 + wm * WM + 2 * q, sg.n0 + wn * WN + r, inside);
+        return gpos;
+      }
+    }
     load_c_block(gpos);
-    return ep.blas ? gpos : gpos + CS;
+    return ep.blas ? gpos : gpos + CSR;
   };
   uint32_t g = 0;  // ring position (C blocks and slabs consumed so far)
   int cur = seg_first();
@@ -683,7 +731,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           // shared-memory reads overlap the global write-back.
           const uint32_t gn = g + NS;
           const bool pre = has_next && nsg.from_c;
-          if (pre)
+          const bool n_inside = CG && pre && c_inside(nsg);
+          const int nrow0 = nsg.m0 + wm * WM + 2 * q, ncol0 = nsg.n0 + wn * WN + r;
+          if (!CG && pre)
             for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(gn + cs) % STAGES], ((gn + cs) / STAGES) & 1);
 #pragma unroll
           for (int i = 0; i < FM; i += 2)
@@ -701,16 +751,22 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
               if (pre) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                  const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
-                  acc[i + h][j][0] = v.x;
-                  acc[i + h][j][1] = v.y;
+                  if constexpr (CG) {
+                    load_c_pair(i + h, j, nrow0, ncol0, n_inside);
+                  } else {
+                    const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
+                    acc[i + h][j][0] = v.x;
+                    acc[i + h][j][1] = v.y;
+                  }
                 }
               }
             }
           if (pre) {
-            __syncwarp();
-            if (lane == 0)
-              for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(gn + cs) % STAGES]);
+            if constexpr (!CG) {
+              __syncwarp();
+              if (lane == 0)
+                for (int cs = 0; cs < CS; ++cs) mbar_arrive(&empty_bar[(gn + cs) % STAGES]);
+            }
             c_loaded = true;
           }
           stored = true;
@@ -740,7 +796,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         }
     }
     g += NS;
-    if (has_next) g = c_loaded ? g + CS : init_acc(nsg, g);
+    if (has_next) g = c_loaded ? g + CSR : init_acc(nsg, g);
     TL_MARK(6);
 #ifdef MYD_TIMELINE
     ++unit_ord;
