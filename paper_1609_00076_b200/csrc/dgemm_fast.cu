@@ -81,6 +81,9 @@ __device__ unsigned long long g_fast_prof[8];
 #define PROF_ADD(i, v)
 #endif
 
+#ifndef MYD_BK32_MIN_K
+#define MYD_BK32_MIN_K 1024  // full tiles use 32-deep K slabs from this K on (16 below)
+#endif
 #ifndef MYD_CGLOBAL
 #define MYD_CGLOBAL 1  // full 128x128 tiles read C from global memory (0: through the ring, for A/B timing)
 #endif
@@ -872,7 +875,7 @@ cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, i
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
-        if (K >= 1024)  // long K: deeper slabs, fewer ring handshakes
+        if (K >= MYD_BK32_MIN_K)  // long K: deeper slabs, fewer ring handshakes
           return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
       }
       return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
@@ -887,7 +890,7 @@ cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, i
 // Full-tile slab depth, as launch_split's case 1 picks it.
 template <int VEC>
 constexpr int full_bk(int K) {
-  return (VEC == 2 && K >= 1024) ? 32 : 16;
+  return (VEC == 2 && K >= MYD_BK32_MIN_K) ? 32 : 16;
 }
 
 inline void keep_pool_memory_fast() { keep_pool_memory(); }
