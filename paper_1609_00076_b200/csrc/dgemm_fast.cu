@@ -84,6 +84,9 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_BK32_MIN_K
 #define MYD_BK32_MIN_K 1024  // full tiles use 32-deep K slabs from this K on (16 below)
 #endif
+#ifndef MYD_CGLOBAL_SK
+#define MYD_CGLOBAL_SK 1  // the stream-K kernel's full tiles too (0: ring, for A/B timing)
+#endif
 #ifndef MYD_CGLOBAL
 #define MYD_CGLOBAL 1  // full 128x128 tiles read C from global memory (0: through the ring, for A/B timing)
 #endif
@@ -195,9 +198,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // the C block no longer takes 2 of 3 (BK 32) or 4 of 6 (BK 16) slots at
   // every unit boundary, so slab prefetch keeps going across it.  cfg4
   // 91.4 -> 94.3 %, k = 128 85.5 -> 91.5 %, 8192^3 +0.2 %
-  // (profiles/c_from_global_r01.log).  Narrower units keep the ring path
-  // (measured slower this way); so does the stream-K kernel.
-  constexpr bool CG = MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && !SKM;
+  // (profiles/c_from_global_r01.log); the stream-K kernel's full tiles too
+  // (2048^3, all stream-K, +0.6 %).  Narrower units keep the ring path
+  // (measured slower this way).
+  constexpr bool CG = MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
 
   extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
