@@ -890,3 +890,51 @@ def test_blas_epilogue_under_stream_k(torch_cuda, m, n, k, alpha, beta):
     bound = HEADLINE_C * (k + 2) * EPS * (abs(alpha) * k + abs(beta))
     assert torch.isfinite(got).all()
     assert float((got - want).abs().max()) <= bound
+
+
+def _fuzz_shapes(seed, count):
+    """Seeded random shapes spanning every kernel family: m or n of 1, few
+    rows / columns, ragged tiles, short and long k, padded / odd lds."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        kind = rng.integers(0, 6)
+        if kind == 0:
+            m, n = 1, int(rng.integers(1, 3000))
+        elif kind == 1:
+            m, n = int(rng.integers(1, 3000)), 1
+        elif kind == 2:
+            m, n = int(rng.integers(2, 17)), int(rng.integers(16, 6000))
+        elif kind == 3:
+            m, n = int(rng.integers(4096, 9000)), int(rng.integers(2, 17))
+        else:
+            m, n = int(rng.integers(1, 1500)), int(rng.integers(1, 1500))
+        k = int(rng.choice([1, 3, 15, 16, 17, 64, 255, 256, 700, 1031, 2048]))
+        pads = [int(p) for p in rng.integers(0, 9, size=3)]
+        out.append((m, n, k, m + pads[0], k + pads[1], m + pads[2]))
+    return out
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_fuzz_random_shapes_fast_vs_exact(torch_cuda, seed):
+    """Random shapes (seeded): the default path (whatever kernel family and
+    plan it picks) within the headline bound of the bitwise-oracle exact
+    kernel, every full-tile plan bitwise equal to the default tiled call, and
+    padding canaries intact."""
+    torch = torch_cuda
+    for (m, n, k, lda, ldb, ldc) in _fuzz_shapes(seed, 40):
+        a, b, c, _ = dev_operands(torch, m, n, k, lda, ldb, ldc, canary=-777.25)
+        fast, exact = c.clone(), c.clone()
+        run_dev(torch, m, n, k, a, lda, b, ldb, fast, ldc)
+        run_dev(torch, m, n, k, a, lda, b, ldb, exact, ldc, exact=True)
+        bound = HEADLINE_C * k * EPS * (k + 1)  # |A||B|+|C| <= k + 1 for entries in [-1, 1)
+        mx, i, j = engine.max_abs_diff_device(m, n, fast.data_ptr(), ldc, exact.data_ptr(), ldc, bound)
+        assert i is None, ((m, n, k, lda, ldb, ldc), i, j, mx)
+        if ldc > m:
+            assert bool((fast.view(n, ldc)[:, m:] == -777.25).all()), (m, n, k)
+        tiled = []
+        for strips in (0, 2, 8, 32):
+            cc = c.clone()
+            run_dev(torch, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True)
+            tiled.append(cc)
+        assert all(torch.equal(tiled[0], t) for t in tiled[1:]), (m, n, k, lda, ldb, ldc)
