@@ -1068,11 +1068,16 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       }
     }
     const int rem_n = N % TILE_N;
-    if (rem_n >= 1 && rem_n <= 64 && tiles_n >= 2) {  // edge column out of the raster
+    // Ragged last tile column (any remainder, also N < 128): kept out of the
+    // raster and run as only its valid strips -- round-robin over a raster
+    // that includes empty units would pile the valid ones onto a quarter of
+    // the CTAs when N < 128 (8192 x 32 x 8192: 573 -> ~150 us).
+    if (rem_n >= 1 && tiles_n >= 1) {  // edge column out of the raster
       const long long te = (long long)tiles_m * (tiles_n - 1);
       const long long qe = te / G, re = te % G;
       for (int s : {2, 4, 8}) {
-        const int ns = s == 2 ? 1 : (rem_n + 31) / 32;  // 128x64: 1 strip; 128x32 / 64x32: 32-wide strips
+        const int bn = s == 2 ? 64 : 32;
+        const int ns = (rem_n + bn - 1) / bn;  // valid strips of the 128x64 / 128x32 / 64x32 units
         const long long nonempty = re * s + (long long)tiles_m * (s == 8 ? 2 : 1) * ns;
         const double cost =
             (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
@@ -1124,11 +1129,12 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       }
     }
     const int rem_m = M % TILE_M;
-    if (rem_m >= 1 && rem_m <= 64) {  // ragged last tile row (or a problem < 64 rows) out of the raster
+    if (rem_m >= 1) {  // ragged last tile row (or a problem < 128 rows) out of the raster
       const long long te = (long long)(tiles_m - 1) * tiles_n;
       const long long qe = te / G, re = te % G;
       for (int s : {8, 16}) {
-        const int ms = s == 8 ? 1 : (rem_m + 15) / 16;  // 64x32: 1 sub-row (x 4 strips); 16x128: 16-row sub-rows
+        // valid sub-rows: 64x32 units (x 4 strips per tile column) or 16x128 units
+        const int ms = s == 8 ? (rem_m + 63) / 64 : (rem_m + 15) / 16;
         const long long nonempty = re * per_tile(s) + (long long)tiles_n * ms * (s == 8 ? 4 : 1);
         const double cost =
             (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
