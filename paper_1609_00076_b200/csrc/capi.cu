@@ -114,7 +114,10 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
   if (split == 0) split = tuned_plan(m, n, k, lda, ldb);  // 0 unless my_dgemm_tune chose one
   const bool force_vec1 = (flags & MY_DGEMM_FORCE_VEC1) != 0;
   const bool a_ok = lda % 2 == 0 && (uintptr_t)A % 16 == 0, b_ok = ldb % 2 == 0 && (uintptr_t)B % 16 == 0;
-  if (!force_vec1 && (!a_ok || !b_ok) && (double)m * n * k >= (double)(1 << 24)) {
+  // Worth a scratch copy when the GEMM is big, or when its K chain is long:
+  // a small m x n problem runs K in order on few SMs, and 8-byte staging
+  // costs it ~2x (17 x 64 x 4096: 194 us vs 83 us at m = 64, profiles/shape_scan_r01.log).
+  if (!force_vec1 && (!a_ok || !b_ok) && ((double)m * n * k >= (double)(1 << 24) || k >= 512)) {
     keep_pool_memory();
     // Odd leading dimension (or 8-byte aligned view) of A or B: copy the
     // operand once into an even-ld scratch copy so the bulk-copy staging
