@@ -170,7 +170,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (profiles/c_from_global_r01.log); the stream-K kernel's full tiles too
   // (2048^3, all stream-K, +0.6 %).  Narrower units keep the ring path
   // (measured slower this way).
-  constexpr bool CG = MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
+  constexpr bool CG = CGT && MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
 
   extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
@@ -833,11 +833,10 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>(), bool SKM = false>
-cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
-                       const double *B,
-                       int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
-                       int after_main, cudaStream_t st, const StreamK &sk = StreamK{}) {
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT>
+cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
+                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                          int edge, int after_main, cudaStream_t st, const StreamK &sk) {
   using namespace fast;
   // The opt-in shared-memory size is a per-device function attribute: set it
   // once per (device, instantiation); racing first calls just set it twice.
@@ -847,7 +846,7 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     cudaError_t e =
-        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
@@ -864,11 +863,30 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM>, M, N, K, A, lda, B, ldb, C, ldc,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT>, M, N, K, A, lda, B, ldb, C, ldc,
                                      tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// Full tiles with a 16-byte aligned C run the instantiation that reads C from
+// global memory (CGT); any other C (odd ldc, 8-byte aligned view) runs the
+// ring-staged one, whose 8-byte staging copies hide the latency scalar global
+// loads would expose (16384^2 x 256, ldc odd: 5.43 ms -> 4.45 ms).  A runtime
+// switch inside one kernel cost the aligned case 2-10 %.
+template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>(), bool SKM = false>
+cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
+                       const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
+                       int edge, int after_main, cudaStream_t st, const StreamK &sk = StreamK{}) {
+  const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+  if constexpr (VEC == 2 && BM == 128 && BN == 128) {
+    if (c_aligned)
+      return launch_kernel<VEC, BM, BN, BK, SKM, true>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n,
+                                                       tile0, edge, after_main, st, sk);
+  }
+  return launch_kernel<VEC, BM, BN, BK, SKM, false>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n,
+                                                    tile0, edge, after_main, st, sk);
 }
 
 template <int VEC>
