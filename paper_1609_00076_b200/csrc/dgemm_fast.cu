@@ -202,6 +202,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (2048^3, all stream-K, +0.6 %).  Narrower units keep the ring path
   // (measured slower this way).
   constexpr bool CG = CGT && MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
+  // The full-tile instantiation launched for an unaligned C (odd ldc, see
+  // launch_one): its C columns alternate 16-byte alignment, so every other
+  // column is still staged by bulk copy and stored with 16-byte stores.  Kept
+  // out of the other instantiations, whose code this slows (2-5 %).
+  constexpr bool ODD_C = VEC == 2 && BM == 128 && BN == 128 && !CGT;
 
   extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
@@ -358,6 +363,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
     const int pw = warp - CONSUMER_WARPS;
     const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+    const bool c16 = ODD_C && ((uintptr_t)C % 16 == 0);
 #ifdef MYD_TIMELINE
     if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
 #endif
@@ -397,23 +403,28 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           // outside C stay stale -- their accumulators are never stored.
           constexpr int CW = CPS / PRODUCER_WARPS;
           const int rows = max(0, min(BM, M - m0));  // 0 for a unit wholly below C
-          const bool col_bulk = c_aligned && (rows % 2 == 0);
-          if (!c_bulk && !col_bulk) {
-            for (int c = 0; c < CW; ++c) {
-              const int col = pw * CW + c;
-              if (c_first + col >= N) break;
-              for (int row = lane; row < rows; row += 32)
-                cp_async<8>(cb + col * CP + row, C + (int64_t)(c_first + col) * ldc + m0 + row, 8);
-            }
+          // a column goes by bulk copy when its first valid element is 16-byte
+          // aligned and it holds an even number of rows (with an odd ldc,
+          // every other column of a 16-byte aligned C)
+          auto col_bulk = [&](int gcol) {
+            return c_bulk || (c16 && rows % 2 == 0 && ((((int64_t)gcol * ldc + m0) & 1) == 0));
+          };
+          for (int c = 0; c < CW; ++c) {
+            const int col = pw * CW + c;
+            if (c_first + col >= N) break;
+            if (col_bulk(c_first + col)) continue;
+            for (int row = lane; row < rows; row += 32)
+              cp_async<8>(cb + col * CP + row, C + (int64_t)(c_first + col) * ldc + m0 + row, 8);
           }
           cp_async_mbar_arrive_inc(&full_bar[slot]);
           __syncwarp();
           int valid_cols = min(CW, N - c_first - pw * CW);
           valid_cols = (valid_cols < 0 || rows == 0) ? 0 : valid_cols;
-          const uint32_t bulk_bytes = (c_bulk || col_bulk) ? (uint32_t)(valid_cols * rows * 8) : 0u;
+          const bool mine = lane < valid_cols && col_bulk(c_first + pw * CW + lane);
+          const uint32_t bulk_bytes = (uint32_t)__popc(__ballot_sync(0xffffffffu, mine)) * rows * 8;
           if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], bulk_bytes);
           __syncwarp();
-          if ((c_bulk || col_bulk) && lane < valid_cols) {
+          if (mine) {
             const int col = pw * CW + lane;
             bulk_g2s(cb + col * CP, C + (int64_t)(c_first + col) * ldc + m0, rows * 8, &full_bar[slot]);
           }
@@ -723,6 +734,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       const int col0 = sg.n0 + wn * WN + r;
       // ---- epilogue: valid region only (padding rows never touched) ----
       const bool vec_store = c_aligned;
+      // odd ldc with a 16-byte aligned base: every other column still takes 16-byte stores
+      const bool c16 = ODD_C && ((uintptr_t)C % 16 == 0);
       bool stored = false;
 #if MYD_EP_SHFL
       // Interior units: lanes r < 4 and r >= 4 (lane ^ 16) swap one pair of
@@ -794,7 +807,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             v0 = ep.beta == 0.0 ? ep.alpha * v0 : fma(ep.alpha, v0, ep.beta * cp[0]);
             if (pair) v1 = ep.beta == 0.0 ? ep.alpha * v1 : fma(ep.alpha, v1, ep.beta * cp[1]);
           }
-          if (pair && vec_store) {
+          if (pair && (vec_store || (c16 && ((((int64_t)col * ldc + row) & 1) == 0)))) {
             *reinterpret_cast<double2 *>(cp) = make_double2(v0, v1);
           } else {
             cp[0] = v0;
