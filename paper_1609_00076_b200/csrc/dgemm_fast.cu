@@ -81,6 +81,10 @@ __device__ unsigned long long g_fast_prof[8];
 #define PROF_ADD(i, v)
 #endif
 
+#ifndef MYD_SKIP_ZERO_KSTEPS
+#define MYD_SKIP_ZERO_KSTEPS 0  // A/B knob: skip the all-zero k-steps of a ragged last K slab (a runtime
+                                // break in the unrolled k-step loop costs the aligned shapes 0.3-4 %: off)
+#endif
 #ifndef MYD_BK32_MIN_K
 #define MYD_BK32_MIN_K 1024  // full tiles use 32-deep K slabs from this K on (16 below)
 #endif
@@ -684,8 +688,17 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       const int nslot = (gs + 1) % STAGES;
       const uint32_t nparity = ((gs + 1) / STAGES) & 1;
       bool next_ready = true;
+#if MYD_SKIP_ZERO_KSTEPS
+      // a ragged last K slab: its k-steps past K hold only the zero fill, so
+      // they are skipped (bitwise the same for every plan and k-chunking: the
+      // skip depends on K alone; it only keeps a -0 accumulator at -0)
+      const int kvalid = (sg.kb + kt == KT - 1) ? (K - (KT - 1) * BK + 3) / 4 : KSTEPS;
+#endif
 #pragma unroll
       for (int kk = 0; kk < KSTEPS; ++kk) {
+#if MYD_SKIP_ZERO_KSTEPS
+        if (kk > 0 && kk >= kvalid) break;
+#endif
         const int cur_buf = kk & 1;
         // Probe the next slab's barrier early; its latency hides behind DMMAs.
         if (kk == PROBE_STEP && kt + 1 < NS) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
