@@ -82,8 +82,7 @@ __device__ unsigned long long g_fast_prof[8];
 #endif
 
 #ifndef MYD_SKIP_ZERO_KSTEPS
-#define MYD_SKIP_ZERO_KSTEPS 0  // A/B knob: skip the all-zero k-steps of a ragged last K slab (a runtime
-                                // break in the unrolled k-step loop costs the aligned shapes 0.3-4 %: off)
+#define MYD_SKIP_ZERO_KSTEPS 1  // ragged-K instantiation skips the all-zero k-steps of the last K slab (0: off)
 #endif
 #ifndef MYD_BK32_MIN_K
 #define MYD_BK32_MIN_K 1024  // full tiles use 32-deep K slabs from this K on (16 below)
@@ -174,7 +173,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -688,17 +687,18 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       const int nslot = (gs + 1) % STAGES;
       const uint32_t nparity = ((gs + 1) / STAGES) & 1;
       bool next_ready = true;
-#if MYD_SKIP_ZERO_KSTEPS
-      // a ragged last K slab: its k-steps past K hold only the zero fill, so
-      // they are skipped (bitwise the same for every plan and k-chunking: the
-      // skip depends on K alone; it only keeps a -0 accumulator at -0)
-      const int kvalid = (sg.kb + kt == KT - 1) ? (K - (KT - 1) * BK + 3) / 4 : KSTEPS;
-#endif
+      // RK (K not a multiple of BK, its own instantiation: a runtime exit in
+      // the unrolled k-step loop costs the other shapes 0.3-4 %): the k-steps
+      // of the last slab past K hold only the zero fill and are skipped.
+      // Every unit shape, plan and k-chunking of a problem computes the same
+      // k-steps (those holding at least one k < K; chunks are multiples of
+      // 16), so C stays bitwise plan-invariant, the sign of zeros included.
+      const int kvalid = (RK && sg.kb + kt == KT - 1) ? (K - (KT - 1) * BK + 3) / 4 : KSTEPS;
 #pragma unroll
       for (int kk = 0; kk < KSTEPS; ++kk) {
-#if MYD_SKIP_ZERO_KSTEPS
-        if (kk > 0 && kk >= kvalid) break;
-#endif
+        if constexpr (RK) {
+          if (kk > 0 && kk >= kvalid) break;
+        }
         const int cur_buf = kk & 1;
         // Probe the next slab's barrier early; its latency hides behind DMMAs.
         if (kk == PROBE_STEP && kt + 1 < NS) next_ready = mbar_try_wait(&full_bar[nslot], nparity);
@@ -859,7 +859,7 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -872,7 +872,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     cudaError_t e =
-        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
@@ -889,7 +889,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT>, M, N, K, A, lda, B, ldb, C, ldc,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, M, N, K, A, lda, B, ldb, C, ldc,
                                      tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
@@ -906,13 +906,23 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
                        const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                        int edge, int after_main, cudaStream_t st, const StreamK &sk = StreamK{}) {
   const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
+  // K with a ragged last slab holding at least one all-zero k-step: the RK
+  // instantiation skips them -- for every unit shape, so the set of k-steps
+  // each element sees (hence C, bitwise, even the sign of a zero) does not
+  // depend on the plan or on which kernel a shard's tile lands in.
+  const bool rk = MYD_SKIP_ZERO_KSTEPS && K % BK != 0 && BK - K % BK >= 4;
+#define MYD_LAUNCH(CGT_, RK_)                                                                                   \
+  return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, \
+                                                        tile0, edge, after_main, st, sk)
   if constexpr (VEC == 2 && BM == 128 && BN == 128) {
-    if (c_aligned)
-      return launch_kernel<VEC, BM, BN, BK, SKM, true>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n,
-                                                       tile0, edge, after_main, st, sk);
+    if (c_aligned) {
+      if (rk) MYD_LAUNCH(true, true);
+      MYD_LAUNCH(true, false);
+    }
   }
-  return launch_kernel<VEC, BM, BN, BK, SKM, false>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n,
-                                                    tile0, edge, after_main, st, sk);
+  if (rk) MYD_LAUNCH(false, true);
+  MYD_LAUNCH(false, false);
+#undef MYD_LAUNCH
 }
 
 template <int VEC>

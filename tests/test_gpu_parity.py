@@ -938,3 +938,25 @@ def test_fuzz_random_shapes_fast_vs_exact(torch_cuda, seed):
             run_dev(torch, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True)
             tiled.append(cc)
         assert all(torch.equal(tiled[0], t) for t in tiled[1:]), (m, n, k, lda, ldb, ldc)
+
+
+@pytest.mark.parametrize("m,n,k,lds", [(300, 260, 100, (300, 100, 300)), (257, 300, 20, (257, 21, 259)),
+                                       (1024, 1024, 1028, (1024, 1028, 1024))])
+def test_signed_zero_is_plan_invariant_and_matches_the_oracle(torch_cuda, m, n, k, lds):
+    """C = -0, A = +0, B = -1: every real product is -0, so the reference's
+    loop (acc = acc + a*b from acc = C) keeps -0.  K is ragged, so the last
+    K slab carries all-zero k-steps; the kernels skip them in every unit
+    shape and plan (computing them would turn -0 into +0), so every plan
+    returns -0 everywhere, bitwise the exact kernel."""
+    torch = torch_cuda
+    lda, ldb, ldc = lds
+    a = torch.zeros(lda * k, dtype=torch.float64, device="cuda")
+    b = torch.full((ldb * n,), -1.0, dtype=torch.float64, device="cuda")
+    c = torch.full((ldc * n,), -0.0, dtype=torch.float64, device="cuda")
+    ce = c.clone()
+    run_dev(torch, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    assert bool(torch.signbit(ce.view(n, ldc)[:, :m]).all())
+    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40):
+        cc = c.clone()
+        run_dev(torch, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True)
+        assert bool(torch.signbit(cc.view(n, ldc)[:, :m]).all()), strips
