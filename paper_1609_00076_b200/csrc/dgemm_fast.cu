@@ -31,11 +31,12 @@
 // and only the valid region is stored back.  The DMMA computes the C^T block
 // (B^T A^T) so each thread's accumulator pair is 16 contiguous bytes of C.
 //
-// Per-element arithmetic (k grouped in fours from p = 0, one DMMA per group,
-// groups in ascending order, accumulator starting at C) does not depend on
-// the unit shape, the tile position, the K-slab depth, the launch plan or
-// which CTA runs which slabs, so every plan (stream-K included) and every
-// k-chunking at multiples of 16 gives bitwise the same C.
+// Per-element arithmetic (k grouped in fours from p = 0, one DMMA per group
+// that holds at least one k < K, groups in ascending order, accumulator
+// starting at C) does not depend on the unit shape, the tile position, the
+// K-slab depth, the launch plan or which CTA runs which slabs, so every plan
+// (stream-K included) and every k-chunking at multiples of 16 gives bitwise
+// the same C, down to the sign of zeros.
 #include <algorithm>
 #include <cstdlib>
 #include <atomic>
