@@ -1094,8 +1094,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // on whole-call timings of 256-4096^3, tools/midsize_plans.py,
     // profiles/midsize_plans_r01.log, where 4 us instead of 2 stops 64x32
     // units winning at 768-1280^3 by a model margin they do not have; 16x128
-    // units, LDGSTS-staged, refitted on tools/rows16_probe.py: e 0.74, b 0.5)
-    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 0.5 : 4.0))); };
+    // units, LDGSTS-staged, refitted on tools/rows16_probe.py and short-K
+    // ragged rows (tools/plans_for.py): e 0.74, b 2)
+    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 2.0 : 4.0))); };
     auto unit_us = [&](int s) {
       const double ideal = 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3;
       const double e = s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : (s == 16 ? 0.740 : 0.977)));
