@@ -85,6 +85,9 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_SKIP_ZERO_KSTEPS
 #define MYD_SKIP_ZERO_KSTEPS 1  // ragged-K instantiation skips the all-zero k-steps of the last K slab (0: off)
 #endif
+#ifndef MYD_ROWS16_BK
+#define MYD_ROWS16_BK 32  // K-slab depth of the 16x128 units
+#endif
 #ifndef MYD_BK32_MIN_K
 #define MYD_BK32_MIN_K 1024  // full tiles use 32-deep K slabs from this K on (16 below)
 #endif
@@ -941,7 +944,7 @@ cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, i
     case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
     case 4: return launch_one<VEC, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
     case 16:  // 16x128 units (8 per tile, stacked in m): few-row problems and ragged last tile rows
-      return launch_one<VEC, 16, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+      return launch_one<VEC, 16, 128, MYD_ROWS16_BK>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
     default: return launch_one<VEC, 64, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
   }
 }
