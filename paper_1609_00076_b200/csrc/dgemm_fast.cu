@@ -38,6 +38,7 @@
 // (stream-K included) and every k-chunking at multiples of 16 gives bitwise
 // the same C, down to the sign of zeros.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <atomic>
 #include <type_traits>
@@ -1209,6 +1210,14 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       }
     }
   }
+  static const bool trace = [] {  // MY_DGEMM_PLAN_TRACE=1: print each call's launch plan to stderr
+    const char *v = getenv("MY_DGEMM_PLAN_TRACE");
+    return v && *v && *v != '0';
+  }();
+  if (trace)
+    fprintf(stderr, "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d q=%lld raster=%dx%d edge=%d\n",
+            M, N, K, (long long)tiles_m, tiles_n, streamk ? "stream-K" : "units", split, sk_split, q, raster_m,
+            raster_n, edge);
   if (streamk) {
     SkWorkspace ws;
     cudaError_t e = ws.alloc((int)G, stream);
