@@ -188,6 +188,7 @@ MY_DGEMM_API int my_dgemm_set_max_ctas(int n);
 #define MY_DGEMM_PATH_FEW_COLS 3 /* 2 <= n <= 16, m >= 4096 */
 #define MY_DGEMM_PATH_FEW_ROWS 4 /* 2 <= m <= 8 (n-dependent, see my_dgemm_path) */
 #define MY_DGEMM_PATH_EXACT 5    /* MY_DGEMM_EXACT */
+#define MY_DGEMM_PATH_ROWS_DMMA 6 /* 2 <= m <= 32, wide n: B streamed into DMMA fragments */
 MY_DGEMM_API int my_dgemm_path(int m, int n, unsigned flags);
 
 /*

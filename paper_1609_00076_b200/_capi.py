@@ -25,7 +25,7 @@ FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
 FORCE_STREAMK = 0x800
 IPC_HANDLE_BYTES = 64
-PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT = range(6)
+PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT, PATH_ROWS_DMMA = range(7)
 
 
 def FORCE_PATH(p: int) -> int:  # noqa: N802 - mirrors the C macro

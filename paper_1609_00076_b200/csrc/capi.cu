@@ -33,6 +33,8 @@ cudaError_t launch_gemm_nsmall(int M, int N, int K, const double *A, int64_t lda
                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_gemm_msmall(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep);
+cudaError_t launch_gemm_rows_dmma(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                                  double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep);
 cudaError_t launch_fill_random(double *out, int64_t m, int64_t n, int64_t ld, uint64_t seed, int64_t col0,
                                cudaStream_t stream);
 cudaError_t launch_copy2d(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst, int64_t ldd,
@@ -64,19 +66,22 @@ void keep_pool_memory() {
 }
 
 // Which kernel a call uses (my_dgemm_path): the bandwidth kernels take the
-// shapes with one short dimension -- m == 1; few rows (m <= 4 with
-// n <= 65536, m <= 8 with n <= 4096: beyond that the tiled kernel's 16x128
-// units win, tools/fewrows_vs_tiled.py); n == 1; few columns (n <= 16 with m >= 4096) -- every other
-// shape is tiled.  Sharded drivers pass the whole problem's path to every
-// shard (MY_DGEMM_FORCE_PATH), so a narrow shard never changes kernel.
-// Measurements: tools/nsmall_probe.py, tools/msmall_probe.py.
+// shapes with one short dimension -- m == 1; few rows: m <= 4 with
+// n <= 65536 on the FMA kernel, 5 <= m <= 16 on the DMMA row kernel (1.1-2x
+// the tiled kernel's 16x128 units, which use only n/128 SMs;
+// profiles/rows_dmma_r01.log); n == 1; few columns (n <= 16 with m >= 4096)
+// -- every other shape is tiled.  Sharded drivers pass the whole problem's
+// path to every shard (MY_DGEMM_FORCE_PATH), so a narrow shard never changes
+// kernel.  Measurements: tools/nsmall_probe.py, tools/msmall_probe.py,
+// tools/rows_dmma_probe.py.
 int path_kind(int m, int n, unsigned flags) {
   if (flags & MY_DGEMM_EXACT) return MY_DGEMM_PATH_EXACT;
   if (flags & MY_DGEMM_PATH_MASK) return (int)((flags & MY_DGEMM_PATH_MASK) >> 8) - 1;
   if (flags & MY_DGEMM_FORCE_TILED) return MY_DGEMM_PATH_TILED;
   if (m == 1) return MY_DGEMM_PATH_GEMV_M1;
-  if ((m <= 4 && n <= 65536) || (m <= 8 && n <= 4096)) return MY_DGEMM_PATH_FEW_ROWS;
+  if (m <= 4 && n <= 65536) return MY_DGEMM_PATH_FEW_ROWS;
   if (n == 1) return MY_DGEMM_PATH_GEMV_N1;
+  if (m >= 5 && m <= 16) return MY_DGEMM_PATH_ROWS_DMMA;
   if (n <= 16 && m >= 4096) return MY_DGEMM_PATH_FEW_COLS;
   return MY_DGEMM_PATH_TILED;
 }
@@ -90,6 +95,7 @@ bool path_fits(int m, int n, unsigned flags) {
     case MY_DGEMM_PATH_GEMV_M1: return m == 1;
     case MY_DGEMM_PATH_FEW_COLS: return n <= 16;
     case MY_DGEMM_PATH_FEW_ROWS: return m <= 16;
+    case MY_DGEMM_PATH_ROWS_DMMA: return m <= 32;
     default: return false;
   }
 }
@@ -101,6 +107,7 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
     case MY_DGEMM_PATH_EXACT: return launch_dgemm_exact(m, n, k, A, lda, B, ldb, C, ldc, st);
     case MY_DGEMM_PATH_GEMV_M1: return launch_gemv_m1(n, k, A, lda, B, ldb, C, ldc, st, ep);
     case MY_DGEMM_PATH_FEW_ROWS: return launch_gemm_msmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
+    case MY_DGEMM_PATH_ROWS_DMMA: return launch_gemm_rows_dmma(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
     case MY_DGEMM_PATH_GEMV_N1: return launch_gemv_n1(m, k, A, lda, B, C, st, ep);
     case MY_DGEMM_PATH_FEW_COLS: return launch_gemm_nsmall(m, n, k, A, lda, B, ldb, C, ldc, st, ep);
     default: break;

@@ -11,6 +11,7 @@
 // (goto.py:187-239); on the GPU they are bandwidth problems, not DMMA ones.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -304,6 +305,114 @@ __global__ void __launch_bounds__(32 * WARPS)
 }
 
 // ---------------------------------------------------------------------------
+// 2 <= m <= 8*MT with a wide B (few rows on the FP64 tensor path).  B is the
+// big operand and streams once from HBM straight into DMMA fragments: a CTA
+// owns 8*CT columns, its WARPS warps split k into contiguous slices of k4
+// groups, and per k4 group a warp loads CT B fragments (8 columns x 32
+// contiguous bytes: full sectors, evict-first) and MT A fragments (8 rows x 4
+// k; A is m*k*8 bytes and stays in L2) and issues CT*MT DMMA.8x8x4 computing
+// the C^T block (B^T A^T).  The main loop touches no shared memory and keeps
+// U k4 groups of loads in flight per warp, so the SM is bound by HBM, not by
+// operand staging (the FMA kernel above is bound by its shared-memory A reads
+// from m = 8 on).  Out-of-range columns / rows read a clamped (valid) address
+// and are never stored; the partials of the WARPS slices meet in shared
+// memory and are added in warp order, then onto C.  The per-element order
+// depends only on K, so C is bitwise invariant to any split of the columns.
+// ---------------------------------------------------------------------------
+template <int MT, int CT, int WARPS, int U, bool VB>
+__global__ void __launch_bounds__(32 * WARPS)
+    gemm_rows_dmma_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda,
+                          const double *__restrict__ B, int64_t ldb, double *__restrict__ C, int64_t ldc,
+                          Epilogue ep) {
+  static_assert(!VB || U % 2 == 0, "16-byte B loads take k in pairs");
+  extern __shared__ double part[];  // [WARPS][8*CT columns][8*MT rows]
+  constexpr int NB = 8 * CT, MB = 8 * MT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = lane >> 2, q = lane & 3;  // fragment row (a column j of C, or a row i) and k in the group
+  const int64_t j0 = (int64_t)blockIdx.x * NB;
+  const int G = (K + 3) >> 2, per = (G + WARPS - 1) / WARPS;
+  const int g0 = min(G, warp * per), g1 = min(G, g0 + per), gfull = min(g1, K >> 2);
+  const double *bp[CT];
+  const double *ap[MT];
+#pragma unroll
+  for (int ct = 0; ct < CT; ++ct) bp[ct] = B + min(j0 + 8 * ct + r, (int64_t)N - 1) * ldb;
+#pragma unroll
+  for (int rt = 0; rt < MT; ++rt) ap[rt] = A + min(8 * rt + r, M - 1);
+  double acc[MT][CT][2];
+#pragma unroll
+  for (int rt = 0; rt < MT; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) acc[rt][ct][0] = acc[rt][ct][1] = -0.0;  // the additive identity: -0 sums stay -0
+  // Main loop: batches of U full k4 groups (4U consecutive k).  Within a
+  // batch, slot q of DMMA u holds k = k0 + U q + u, so a lane's U B values
+  // of a column are contiguous (VB: U/2 16-byte loads) and a column's 4U
+  // values are one contiguous 32U-byte run per warp batch.
+  int g = g0;
+  for (; g + U <= gfull; g += U) {
+    const int64_t k0 = 4 * (int64_t)g + U * q;
+    double fb[U][CT], fa[U][MT];
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) {
+      if constexpr (VB) {
+#pragma unroll
+        for (int u = 0; u < U; u += 2) {
+          const double2 v = __ldcs(reinterpret_cast<const double2 *>(bp[ct] + k0 + u));
+          fb[u][ct] = v.x;
+          fb[u + 1][ct] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) fb[u][ct] = __ldcs(bp[ct] + k0 + u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int rt = 0; rt < MT; ++rt) fa[u][rt] = __ldg(ap[rt] + (k0 + u) * lda);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+        for (int rt = 0; rt < MT; ++rt) dmma_884(acc[rt][ct][0], acc[rt][ct][1], fb[u][ct], fa[u][rt]);
+  }
+  for (; g < g1; ++g) {
+    const bool kv = 4 * g + q < K;  // only the last group of k can be partial
+    double fb[CT], fa[MT];
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct) fb[ct] = kv ? __ldcs(bp[ct] + 4 * g + q) : 0.0;
+#pragma unroll
+    for (int rt = 0; rt < MT; ++rt) fa[rt] = kv ? __ldg(ap[rt] + (int64_t)(4 * g + q) * lda) : -0.0;  // (+0)(-0) = -0
+#pragma unroll
+    for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+      for (int rt = 0; rt < MT; ++rt) dmma_884(acc[rt][ct][0], acc[rt][ct][1], fb[ct], fa[rt]);
+  }
+  // lane holds C[i = 8rt + 2q + {0,1}][j = j0 + 8ct + r]
+  double *pw = part + (size_t)warp * NB * MB;
+#pragma unroll
+  for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+    for (int rt = 0; rt < MT; ++rt)
+      *reinterpret_cast<double2 *>(pw + (8 * ct + r) * MB + 8 * rt + 2 * q) =
+          make_double2(acc[rt][ct][0], acc[rt][ct][1]);
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * MB; e += 32 * WARPS) {
+    const int i = e % MB;
+    const int64_t j = j0 + e / MB;
+    if (i >= M || j >= N) continue;
+    double s = part[e];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) s += part[(size_t)w * NB * MB + e];
+    double *cp = C + j * ldc + i;
+    if (!ep.blas)
+      *cp = *cp + s;
+    else
+      *cp = ep.beta == 0.0 ? ep.alpha * s : fma(ep.alpha, s, ep.beta * *cp);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // m == 1.  Teams of TEAM warps own columns (round-robin over all teams of the
 // grid); warp t of a team reduces k-quarter t of the column with lane-strided
 // coalesced loads, then the team combines its TEAM partials in order behind
@@ -485,6 +594,74 @@ cudaError_t launch_gemm_msmall(int M, int N, int K, const double *A, int64_t lda
   if (M <= 4) return launch_msmall_cols<4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
   if (M <= 8) return launch_msmall_cols<8>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
   return launch_msmall_cols<16>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+}
+
+namespace {
+#ifndef MYD_RD_WARPS
+#define MYD_RD_WARPS 8
+#endif
+// k4 groups per load batch: 2 for m <= 8, 4 for m <= 16, 8 for m <= 32
+// (tools/rows_dmma_probe.py, profiles/rows_dmma_r01.log); MYD_RD_U pins it
+#ifdef MYD_RD_U
+template <int MT> constexpr int rd_u() { return MYD_RD_U; }
+#else
+template <int MT> constexpr int rd_u() { return MT == 1 ? 2 : (MT == 2 ? 4 : 8); }
+#endif
+template <int MT, int CT, bool VB>
+cudaError_t launch_rows_dmma_t(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                               double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  constexpr int WARPS = MYD_RD_WARPS, U = rd_u<MT>();
+  constexpr size_t smem = (size_t)WARPS * 8 * CT * 8 * MT * 8;
+  if constexpr (smem > 48 * 1024) {
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_rows_dmma_kernel<MT, CT, WARPS, U, VB>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr_done.fetch_or(bit, std::memory_order_release);
+    }
+  }
+  const int64_t grid = (N + 8 * CT - 1) / (8 * CT);
+  gemm_rows_dmma_kernel<MT, CT, WARPS, U, VB><<<(unsigned)grid, 32 * WARPS, smem, stream>>>(M, N, K, A, lda, B, ldb,
+                                                                                            C, ldc, ep);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int MT>
+cudaError_t launch_rows_dmma_ct(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                                double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  // Wider column blocks re-read A from L2 less often (N / (8 CT) times);
+  // narrower ones give more CTAs: 32 columns per CTA for m > 8 once that
+  // still covers every SM, else 16.  MY_DGEMM_RD_CT overrides (A/B only).
+  static const int force_ct = [] {
+    const char *v = getenv("MY_DGEMM_RD_CT");
+    return v ? atoi(v) : 0;
+  }();
+  const int sms = sm_count_skinny();
+  int ct = force_ct;
+  if (ct != 1 && ct != 2 && ct != 4) ct = MT > 1 && N >= 32 * sms ? 4 : 2;
+  // 16-byte B loads need an even ldb and a 16-byte aligned B
+  if ((ldb & 1) == 0 && (reinterpret_cast<uintptr_t>(B) & 15) == 0) {
+    if (ct == 4) return launch_rows_dmma_t<MT, 4, true>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+    if (ct == 2) return launch_rows_dmma_t<MT, 2, true>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+    return launch_rows_dmma_t<MT, 1, true>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  }
+  if (ct == 4) return launch_rows_dmma_t<MT, 4, false>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (ct == 2) return launch_rows_dmma_t<MT, 2, false>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_rows_dmma_t<MT, 1, false>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+}
+}  // namespace
+
+// 2 <= M <= 32 rows on DMMA (dispatch checks).
+cudaError_t launch_gemm_rows_dmma(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
+                                  double *C, int64_t ldc, cudaStream_t stream, const Epilogue &ep) {
+  if (M <= 8) return launch_rows_dmma_ct<1>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  if (M <= 16) return launch_rows_dmma_ct<2>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
+  return launch_rows_dmma_ct<4>(M, N, K, A, lda, B, ldb, C, ldc, stream, ep);
 }
 
 cudaError_t launch_gemv_m1(int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,

@@ -200,20 +200,21 @@ def test_set_max_ctas_roundtrip(lib):
     assert lib.my_dgemm_set_max_ctas(0) == 0
 
 
-FP = [(p + 1) << 8 for p in range(6)]  # MY_DGEMM_FORCE_PATH(p)
+FP = [(p + 1) << 8 for p in range(7)]  # MY_DGEMM_FORCE_PATH(p)
 
 
 @pytest.mark.parametrize("m,n,flags,want", [
     (8192, 8192, 0, 0), (8192, 1, 0, 1), (1, 8192, 0, 2), (1, 1, 0, 2), (8192, 16, 0, 3), (4095, 16, 0, 0),
-    (8192, 17, 0, 0), (4, 65536, 0, 4), (4, 65537, 0, 0), (5, 4096, 0, 4), (8, 4097, 0, 0), (2, 3, 0, 4),
-    (9, 8192, 0, 0), (8, 1, 0, 4), (100, 1, 0, 1),
+    (8192, 17, 0, 0), (4, 65536, 0, 4), (4, 65537, 0, 0), (5, 4096, 0, 6), (8, 4097, 0, 6), (2, 3, 0, 4),
+    (9, 8192, 0, 6), (16, 100000, 0, 6), (17, 8192, 0, 0), (8, 1, 0, 1), (4, 1, 0, 4), (100, 1, 0, 1),
     (8192, 1, 0x4, 0), (4, 4, 0x4, 0), (4, 4, 0x2, 5),
     (8192, 1, FP[0], 0), (100, 1, FP[1], 1), (1, 50, FP[2], 2), (9000, 12, FP[3], 3), (16, 99999, FP[4], 4),
-    (100, 2, FP[1], -3), (2, 100, FP[2], -3), (100, 17, FP[3], -3), (17, 100, FP[4], -3),
+    (32, 7, FP[6], 6), (2, 9999, FP[6], 6),
+    (100, 2, FP[1], -3), (2, 100, FP[2], -3), (100, 17, FP[3], -3), (17, 100, FP[4], -3), (33, 100, FP[6], -3),
 ])
 def test_path_kind_rules(lib, m, n, flags, want):
     """my_dgemm_path: which kernel family a shape runs on (0 tiled, 1 n == 1,
-    2 m == 1, 3 few columns, 4 few rows, 5 exact; FORCE_TILED = 0x4;
+    2 m == 1, 3 few columns, 4 few rows (FMA), 5 exact, 6 few rows (DMMA); FORCE_TILED = 0x4;
     MY_DGEMM_FORCE_PATH(p) forces a family that suits the shape, else -3)."""
     assert lib.my_dgemm_path(m, n, flags) == want
     assert lib.my_dgemm_path(0, n, flags) == -1

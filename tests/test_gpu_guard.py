@@ -77,6 +77,7 @@ SCRIPT = textwrap.dedent(r"""
         (1000, 1100, 300, 1000, 300, 1000), (777, 1029, 201, 781, 205, 780), (2048, 2048, 512, 2048, 512, 2048),
         (4093, 4099, 200, 4100, 202, 4096), (4100, 3000, 130, 4101, 131, 4102), (37, 53, 71, 44, 76, 40),
         (1, 700, 300, 3, 301, 2), (700, 1, 300, 701, 303, 703), (6, 3000, 90, 7, 91, 6), (5000, 7, 60, 5001, 61, 5000),
+        (16, 5000, 77, 17, 79, 18), (12, 333, 5, 12, 5, 12), (9, 6000, 64, 9, 64, 9),
     ]
     for at_end in (True, False):
         for (m, n, k, lda, ldb, ldc) in cases:

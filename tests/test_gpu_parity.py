@@ -848,27 +848,98 @@ def test_few_columns_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     (2, 4100, 100, 2, 100, 2),
 ])
 def test_few_rows_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
-    """2 <= m <= 16 with a wide B runs on the few-row kernel: within the
-    headline bound of the exact kernel, deterministic, padding untouched, and
-    the BLAS epilogue (beta = 0 on a NaN-filled C) through it."""
+    """2 <= m <= 16 on the FMA few-row kernel (PATH_FEW_ROWS; the default up
+    to m = 4): within the headline bound of the exact kernel, deterministic,
+    padding untouched, and the BLAS epilogue (beta = 0 on a NaN-filled C)
+    through the default path."""
     a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
     cf, ce = c.clone(), c.clone()
-    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc, path=_capi.PATH_FEW_ROWS)
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
     bound = HEADLINE_C * k * EPS * (k + 1)
     mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
     assert i is None, (i, j, mx)
     again = c.clone()
-    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc)
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc, path=_capi.PATH_FEW_ROWS)
     assert torch_cuda.equal(again, cf)
     if ldc > m:
         assert np.all(cf.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
     cn = torch_cuda.full_like(c, float("nan"))
     engine.dgemm("N", "N", m, n, k, 1.0, a.view(-1), lda, b.view(-1), ldb, 0.0, cn, ldc)
     torch_cuda.cuda.synchronize()
-    prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
+    cd = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cd, ldc)  # default path (m > 4: the DMMA row kernel)
+    prod = (cd - c).cpu().numpy().reshape(n, ldc)[:, :m]
     got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
     assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (8, 8192, 3000, 8, 3000, 8),
+    (16, 8192, 700, 16, 701, 19),           # odd ldb: 8-byte B loads
+    (5, 5000, 1001, 9, 1004, 8),            # k % 4 == 1, ragged column blocks
+    (12, 4100, 3, 12, 3, 12),               # k < 4: only the partial group
+    (16, 33, 8192, 16, 8192, 16),           # one CTA, long k split over the warps
+    (24, 2000, 515, 27, 516, 25),           # forced: 17..32 rows (4 row tiles)
+    (32, 9000, 256, 32, 256, 32),
+    (2, 3000, 64, 2, 64, 2),
+])
+def test_rows_dmma_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
+    """The DMMA row kernel (PATH_ROWS_DMMA; default for 5 <= m <= 16, forced
+    up to 32 rows): within the headline bound of the exact kernel,
+    deterministic, bitwise invariant to splitting the columns (what the
+    sharded drivers rely on), padding untouched, and the BLAS epilogue
+    (beta = 0 on a NaN-filled C) through it."""
+    torch = torch_cuda
+    P = _capi.PATH_ROWS_DMMA
+    a, b, c, _ = dev_operands(torch, m, n, k, lda, ldb, ldc, canary=-777.25)
+    cf, ce = c.clone(), c.clone()
+    run_dev(torch, m, n, k, a, lda, b, ldb, cf, ldc, path=P)
+    run_dev(torch, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    bound = HEADLINE_C * k * EPS * (k + 1)
+    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
+    assert i is None, (i, j, mx)
+    again = c.clone()
+    run_dev(torch, m, n, k, a, lda, b, ldb, again, ldc, path=P)
+    assert torch.equal(again, cf)
+    # column shards (ragged widths, B and C views at column offsets) give the same bits
+    split = c.clone()
+    j0 = 0
+    for w in (n // 3 + 1, 7, n):
+        w = min(w, n - j0)
+        if w <= 0:
+            break
+        engine.dgemm_device(m, w, k, a.data_ptr(), lda, b.data_ptr() + 8 * j0 * ldb, ldb,
+                            split.data_ptr() + 8 * j0 * ldc, ldc, torch.cuda.current_stream().cuda_stream, path=P)
+        j0 += w
+    torch.cuda.synchronize()
+    assert torch.equal(split, cf)
+    if ldc > m:
+        assert np.all(cf.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
+    if 5 <= m <= 16:
+        assert engine.path(m, n) == P
+        cd = c.clone()
+        run_dev(torch, m, n, k, a, lda, b, ldb, cd, ldc)
+        assert torch.equal(cd, cf)
+        cn = torch.full_like(c, float("nan"))
+        engine.dgemm("N", "N", m, n, k, 1.0, a.view(-1), lda, b.view(-1), ldb, 0.0, cn, ldc)
+        torch.cuda.synchronize()
+        prod = (cf - c).cpu().numpy().reshape(n, ldc)[:, :m]
+        got = cn.cpu().numpy().reshape(n, ldc)[:, :m]
+        assert np.all(np.isfinite(got)) and np.abs(got - prod).max() <= 2 * bound
+
+
+def test_rows_dmma_keeps_negative_zero(torch_cuda):
+    """C = -0, A = +0, B = -1: every product is -0 and the reference keeps
+    -0 (acc = C, acc += a*b); the row kernel's accumulators start at -0, the
+    additive identity, so -0 survives the slice sum and the add onto C."""
+    torch = torch_cuda
+    m, n, k = 12, 3000, 203
+    a = torch.zeros(m * k, dtype=torch.float64, device="cuda")
+    b = torch.full((k * n,), -1.0, dtype=torch.float64, device="cuda")
+    c = torch.full((m * n,), -0.0, dtype=torch.float64, device="cuda")
+    run_dev(torch, m, n, k, a, m, b, k, c, m, path=_capi.PATH_ROWS_DMMA)
+    assert bool(torch.signbit(c).all())
 
 
 @pytest.mark.parametrize("m,n,k,alpha,beta", [(2048, 2048, 512, 1.5, -0.5), (2048, 2304, 700, 2.0, 0.0),

@@ -103,7 +103,8 @@ def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q):
 
 @pytest.mark.parametrize("shape,lds,k_chunk,overlap", [
     ((37, 300, 71), (44, 76, 40), 32, True),
-    ((16, 129, 50), (16, 50, 16), 16, True),
+    ((16, 129, 50), (16, 50, 16), 16, True),   # few-row path: one k chunk (only the tiled family chunks k)
+    ((20, 129, 50), (20, 50, 21), 16, True),
     ((37, 300, 71), (44, 76, 40), 32, False),
 ])
 def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk, overlap):
@@ -124,7 +125,9 @@ def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk, ove
     lda, ldb, ldc = lds
     a, b, c = oracle.make_padded_operands(42, m, n, k, lda, ldb, ldc, canary=-9.0)
     want = oracle.naive(m, n, k, a, lda, b, ldb, c.copy(), ldc)
-    nchunks = len(k_chunks(k, k_chunk)) if overlap else 1
+    from paper_1609_00076_b200 import _capi, engine
+
+    nchunks = len(k_chunks(k, k_chunk)) if overlap and engine.path(m, n) == _capi.PATH_TILED else 1
     for rank, j0, j1, cl, calls, a_ok in sorted(results, key=lambda t: t[0]):
         assert a_ok, f"rank {rank} did not receive A"
         if j1 > j0:
