@@ -186,9 +186,9 @@ MY_DGEMM_API int my_dgemm_set_max_ctas(int n);
 #define MY_DGEMM_PATH_GEMV_N1 1  /* n == 1 */
 #define MY_DGEMM_PATH_GEMV_M1 2  /* m == 1 */
 #define MY_DGEMM_PATH_FEW_COLS 3 /* 2 <= n <= 16, m >= 4096 */
-#define MY_DGEMM_PATH_FEW_ROWS 4 /* 2 <= m <= 8 (n-dependent, see my_dgemm_path) */
+#define MY_DGEMM_PATH_FEW_ROWS 4 /* 2 <= m <= 4, n <= 65536 (FMA kernel; forced: m <= 16) */
 #define MY_DGEMM_PATH_EXACT 5    /* MY_DGEMM_EXACT */
-#define MY_DGEMM_PATH_ROWS_DMMA 6 /* 2 <= m <= 32, wide n: B streamed into DMMA fragments */
+#define MY_DGEMM_PATH_ROWS_DMMA 6 /* 5 <= m <= 16 (forced: m <= 32): B streamed into DMMA fragments */
 MY_DGEMM_API int my_dgemm_path(int m, int n, unsigned flags);
 
 /*
