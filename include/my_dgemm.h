@@ -95,6 +95,28 @@ MY_DGEMM_API int my_dgemm_blas(char transa, char transb, int m, int n, int k, do
                   const double *B, int ldb, double beta, double *C, int ldc, unsigned flags, void *stream);
 
 /*
+ * GEMM-based level-3 BLAS ("poorman's BLAS",
+ * PAPER.md:1-15): blocked algorithms whose O(n^3) work is my_dgemm_blas
+ * calls on the DMMA kernels, plus small diagonal-block kernels.  Reference-
+ * BLAS argument order, checks (negative status = 1-based index of the bad
+ * argument; the flags argument is the last index) and quick returns.
+ * Device pointers only (flags must hold MY_DGEMM_DEVICE_PTRS; optional
+ * MY_DGEMM_FORCE_TILED), asynchronous on `stream`.
+ *   my_dsyrk: C := alpha op(A) op(A)^T + beta C on the uplo triangle of the
+ *             n x n C (op(A) n x k); the other triangle is never touched.
+ *   my_dtrmm: B := alpha op(A) B (side 'L') or alpha B op(A) (side 'R').
+ *   my_dtrsm: solves op(A) X = alpha B (side 'L') or X op(A) = alpha B
+ *             (side 'R'); X overwrites B.  A triangular (uplo), diag 'U'
+ *             takes its diagonal as 1 without reading it.
+ */
+MY_DGEMM_API int my_dsyrk(char uplo, char trans, int n, int k, double alpha, const double *A, int lda, double beta,
+                          double *C, int ldc, unsigned flags, void *stream);
+MY_DGEMM_API int my_dtrmm(char side, char uplo, char transa, char diag, int m, int n, double alpha, const double *A,
+                          int lda, double *B, int ldb, unsigned flags, void *stream);
+MY_DGEMM_API int my_dtrsm(char side, char uplo, char transa, char diag, int m, int n, double alpha, const double *A,
+                          int lda, double *B, int ldb, unsigned flags, void *stream);
+
+/*
  * jc-sharded piece of a multi-GPU GEMM: the caller's rank computes
  * C[:, j0:j0+nloc] += A[:, p0:p0+kc] * B[p0:p0+kc, j0:j0+nloc] with device
  * pointers already offset by the caller.  Identical to my_dgemm_ex with

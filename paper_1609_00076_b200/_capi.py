@@ -44,6 +44,11 @@ SIGNATURES = {
     "my_dgemm_shard": (_I, [_I, _I, _I, _P, _I, _P, _I, _P, _I, _P]),
     "my_dgemm_blas": (_I, [ctypes.c_char, ctypes.c_char, _I, _I, _I, _D, _P, _I, _P, _I, _D, _P, _I,
                            ctypes.c_uint, _P]),
+    "my_dsyrk": (_I, [ctypes.c_char, ctypes.c_char, _I, _I, _D, _P, _I, _D, _P, _I, ctypes.c_uint, _P]),
+    "my_dtrmm": (_I, [ctypes.c_char, ctypes.c_char, ctypes.c_char, ctypes.c_char, _I, _I, _D, _P, _I, _P, _I,
+                      ctypes.c_uint, _P]),
+    "my_dtrsm": (_I, [ctypes.c_char, ctypes.c_char, ctypes.c_char, ctypes.c_char, _I, _I, _D, _P, _I, _P, _I,
+                      ctypes.c_uint, _P]),
     "my_dgemm_multi": (_I, [_I, _I, _I, _I, _P, _I, _P, _I, _P, _I]),
     "my_dgemm_multi_ex": (_I, [ctypes.POINTER(_I), _I, _I, _I, _I, _P, _I, _P, _I, _P, _I, ctypes.c_uint]),
     "my_dgemm_fill_random": (_I, [_P, _I64, _I64, _I64, _U64, _I64, _P]),

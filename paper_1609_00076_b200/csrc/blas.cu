@@ -74,7 +74,7 @@ static bool is_trans(char t) { return t == 'T' || t == 't' || t == 'C' || t == '
 static bool valid_trans(char t) { return t == 'N' || t == 'n' || is_trans(t); }
 
 // Device-resident BLAS dgemm (asynchronous on st).  Arguments validated.
-static int blas_device(char ta, char tb, int m, int n, int k, double alpha, const double *A, int lda,
+int blas_device(char ta, char tb, int m, int n, int k, double alpha, const double *A, int lda,
                        const double *B, int ldb, double beta, double *C, int ldc, unsigned flags, cudaStream_t st) {
   cudaError_t e;
   if (alpha == 0.0 || k == 0) {

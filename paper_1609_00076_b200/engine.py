@@ -43,6 +43,9 @@ __all__ = [
     "my_dgemm",
     "my_dgemm_multi",
     "set_max_ctas",
+    "dsyrk",
+    "dtrmm",
+    "dtrsm",
     "path",
     "dgemm_device",
     "fill_random_device",
@@ -321,6 +324,47 @@ def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A, lda
                            ctypes.c_void_p(stream) if dev else None)
     _capi.check(st)
     return C
+
+
+def _level3_stream(t, stream):
+    if not _is_device(t):
+        raise ValueError("level-3 routines take CUDA tensors (device pointers)")
+    if stream is None:
+        import torch
+
+        stream = torch.cuda.current_stream(t.device).cuda_stream
+    return ctypes.c_void_p(stream)
+
+
+def dsyrk(uplo: str, trans: str, n: int, k: int, alpha: float, A, lda: int, beta: float, C, ldc: int,
+          stream: int | None = None):
+    """C := alpha op(A) op(A)^T + beta C on the `uplo` triangle (my_dsyrk; GEMM-based
+    level-3 BLAS).  CUDA tensors, asynchronous on `stream`."""
+    st = _level3_stream(C, stream)
+    _capi.check(_capi.load().my_dsyrk(uplo.encode()[:1], trans.encode()[:1], n, k, float(alpha),
+                                      None if A is None else _ptr(A), lda, float(beta), _ptr(C), ldc,
+                                      _capi.DEVICE_PTRS, st))
+    return C
+
+
+def _tri(fn, side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, stream):
+    st = _level3_stream(B, stream)
+    _capi.check(getattr(_capi.load(), fn)(side.encode()[:1], uplo.encode()[:1], transa.encode()[:1],
+                                          diag.encode()[:1], m, n, float(alpha), None if A is None else _ptr(A),
+                                          lda, _ptr(B), ldb, _capi.DEVICE_PTRS, st))
+    return B
+
+
+def dtrmm(side: str, uplo: str, transa: str, diag: str, m: int, n: int, alpha: float, A, lda: int, B, ldb: int,
+          stream: int | None = None):
+    """B := alpha op(A) B (side 'L') or alpha B op(A) (side 'R'), A triangular (my_dtrmm)."""
+    return _tri("my_dtrmm", side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, stream)
+
+
+def dtrsm(side: str, uplo: str, transa: str, diag: str, m: int, n: int, alpha: float, A, lda: int, B, ldb: int,
+          stream: int | None = None):
+    """Solve op(A) X = alpha B (side 'L') or X op(A) = alpha B (side 'R'); X overwrites B (my_dtrsm)."""
+    return _tri("my_dtrsm", side, uplo, transa, diag, m, n, alpha, A, lda, B, ldb, stream)
 
 
 def tune(m: int, n: int, k: int, lda: int | None = None, ldb: int | None = None, ldc: int | None = None,
