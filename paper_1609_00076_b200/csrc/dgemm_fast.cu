@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // the BLAS epilogue reads C at the end instead).  The copies are issued
       // while the consumers finish the previous unit, so the C load is off the
       // critical path and spread in time instead of bursting at unit start.
-      if (CG && !ep.blas && sg.from_c) {
+      if (CG && (!ep.blas || ep.beta != 0.0) && sg.from_c) {  // BLAS: C is read by the epilogue
         const int rows = max(0, min(BM, M - m0));
         const int col = pw * (BN / PRODUCER_WARPS) + lane;
         if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PRODUCER_WARPS && n0 + col < N)
@@ -755,20 +755,41 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // odd ldc with a 16-byte aligned base: every other column still takes 16-byte stores
       const bool c16 = ODD_C && ((uintptr_t)C % 16 == 0);
       bool stored = false;
+      if (ep.blas) {
+        // BLAS epilogue, alpha * (A B) + beta * C (C not read when beta == 0),
+        // applied to the accumulators before any store: with no store between
+        // them the C reads (L2-prefetched at unit start) are all in flight at
+        // once instead of one round trip per fragment behind each store.
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) {
+            const int row = row0 + i * 8, col = col0 + j * 8;
+            double &v0 = acc[i][j][0], &v1 = acc[i][j][1];
+            if (ep.beta == 0.0 || col >= N || row >= M) {
+              v0 *= ep.alpha;
+              v1 *= ep.alpha;
+              continue;
+            }
+            const double *cp = C + (int64_t)col * ldc + row;
+            v0 = fma(ep.alpha, v0, ep.beta * cp[0]);
+            if (row + 1 < M) v1 = fma(ep.alpha, v1, ep.beta * cp[1]);
+          }
+      }
 #if MYD_EP_SHFL
       // Interior units: lanes r < 4 and r >= 4 (lane ^ 16) swap one pair of
       // every two row-fragments so each warp store writes 4 columns x 128
       // contiguous bytes instead of 8 columns x 64: half the cache lines per
       // store instruction, which is what bounds the write-back of a unit.
       if constexpr (FM % 2 == 0) {
-        if (!ep.blas && c_aligned && sg.m0 + BM <= M && sg.n0 + BN <= N) {
+        if (c_aligned && sg.m0 + BM <= M && sg.n0 + BN <= N) {
           const bool lo = r < 4;
           const int rowb = row0 + (lo ? 0 : 8), colb = col0 - (lo ? 0 : 4);
           // The next unit's C block (already staged in the ring) is read into
           // each fragment pair right after that pair is stored, so the
           // shared-memory reads overlap the global write-back.
           const uint32_t gn = g + NS;
-          const bool pre = has_next && nsg.from_c;
+          const bool pre = has_next && nsg.from_c && !ep.blas;  // the BLAS epilogue starts from 0
           const bool n_inside = CG && pre && c_inside(nsg);
           const int nrow0 = nsg.m0 + wm * WM + 2 * q, ncol0 = nsg.n0 + wn * WN + r;
           if (!CG && pre)
@@ -821,10 +842,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           double *cp = C + (int64_t)col * ldc + row;
           double v0 = acc[i][j][0], v1 = acc[i][j][1];
           const bool pair = row + 1 < M;
-          if (ep.blas) {  // BLAS epilogue: alpha * (A B) + beta * C; C is not read when beta == 0
-            v0 = ep.beta == 0.0 ? ep.alpha * v0 : fma(ep.alpha, v0, ep.beta * cp[0]);
-            if (pair) v1 = ep.beta == 0.0 ? ep.alpha * v1 : fma(ep.alpha, v1, ep.beta * cp[1]);
-          }
           if (pair && (vec_store || (c16 && ((((int64_t)col * ldc + row) & 1) == 0)))) {
             *reinterpret_cast<double2 *>(cp) = make_double2(v0, v1);
           } else {
