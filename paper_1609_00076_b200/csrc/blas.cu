@@ -8,8 +8,13 @@
 //   ordered workspace, then the NN kernels (so the per-element arithmetic is
 //   exactly the NN kernels' on the explicitly transposed operand);
 // * alpha == 1 && beta == 1: the my_dgemm contract (accumulator starts at C);
-//   otherwise the BLAS epilogue: alpha * (A B accumulated from 0) + beta * C,
-//   with C never read when beta == 0;
+//   beta == 0: the BLAS epilogue alpha * (A B accumulated from 0), C never
+//   read; any other beta on the tiled kernel: the reference BLAS order --
+//   C := beta C first (skipped for beta == 1), the smaller of op(A), op(B)
+//   scaled by alpha into workspace (netlib's temp = alpha * B(l, j)), then
+//   the contract (the epilogue's read of C after the K loop cost ~370 us
+//   per 8192^2 C, tools/blas_epilogue_probe.py); the bandwidth kernels keep
+//   the epilogue alpha * (A B) + beta * C;
 // * quick returns and alpha == 0 / k == 0 follow the reference BLAS rules.
 #include <algorithm>
 #include <cstdio>
@@ -44,6 +49,14 @@ __global__ void transpose_kernel(int64_t rows, int64_t cols, const double *__res
   }
 }
 
+// dst (rows x cols) := alpha * src
+__global__ void scale_copy_kernel(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
+                                  double *__restrict__ dst, int64_t ldd, double alpha) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+      dst[j * ldd + i] = alpha * src[j * lds + i];
+}
+
 // C := beta * C over the valid region (beta == 0 writes zeros without reading).
 __global__ void scale_kernel(int64_t m, int64_t n, double *__restrict__ C, int64_t ldc, double beta) {
   for (int64_t j = blockIdx.y; j < n; j += gridDim.y)
@@ -70,12 +83,26 @@ static cudaError_t launch_scale(int64_t m, int64_t n, double *C, int64_t ldc, do
   return cudaGetLastError();
 }
 
+static cudaError_t launch_scale_copy(int64_t rows, int64_t cols, const double *src, int64_t lds, double *dst,
+                                     int64_t ldd, double alpha, cudaStream_t st) {
+  const int64_t gx = std::min<int64_t>((rows + 255) / 256, 64), gy = std::min<int64_t>(cols, 65535);
+  scale_copy_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, st>>>(rows, cols, src, lds, dst, ldd, alpha);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int path_kind(int m, int n, unsigned flags);
+
 static bool is_trans(char t) { return t == 'T' || t == 't' || t == 'C' || t == 'c'; }
 static bool valid_trans(char t) { return t == 'N' || t == 'n' || is_trans(t); }
 
 // Device-resident BLAS dgemm (asynchronous on st).  Arguments validated.
+// fold: allow the reference-BLAS order (scale C, scale an operand, then the
+// contract) on the tiled kernel; callers issuing many small updates from one
+// operand (level3.cu) keep the epilogue, which needs no extra pass.
 int blas_device(char ta, char tb, int m, int n, int k, double alpha, const double *A, int lda,
-                       const double *B, int ldb, double beta, double *C, int ldc, unsigned flags, cudaStream_t st) {
+                       const double *B, int ldb, double beta, double *C, int ldc, unsigned flags, cudaStream_t st,
+                       bool fold) {
   cudaError_t e;
   if (alpha == 0.0 || k == 0) {
     if (beta == 1.0) return capi_ok();
@@ -106,6 +133,29 @@ int blas_device(char ta, char tb, int m, int n, int k, double alpha, const doubl
   ep.alpha = alpha;
   ep.beta = beta;
   ep.blas = !(alpha == 1.0 && beta == 1.0);
+  if (fold && ep.blas && beta != 0.0 && path_kind(m, n, flags & ~MY_DGEMM_DEVICE_PTRS) == MY_DGEMM_PATH_TILED) {
+    if (beta != 1.0 && (e = launch_scale(m, n, C, ldc, beta, st)) != cudaSuccess) return capi_cuda_fail(e, "scale C");
+    if (alpha != 1.0) {
+      keep_pool_memory();
+      const bool on_a = (int64_t)m * k <= (int64_t)k * n;  // scale the smaller operand
+      double *&w = on_a ? wa : wb;
+      const double *&op = on_a ? opA : opB;
+      int64_t &ldo = on_a ? lda_op : ldb_op;
+      const int64_t rows = on_a ? m : k, cols = on_a ? k : n;
+      if (!w) {
+        const int64_t ldw = (rows + 1) & ~1LL;
+        if ((e = cudaMallocAsync((void **)&w, (size_t)ldw * cols * 8, st)) != cudaSuccess)
+          return capi_cuda_fail(e, "cudaMallocAsync(alpha op)");
+        if ((e = launch_scale_copy(rows, cols, op, ldo, w, ldw, alpha, st)) != cudaSuccess)
+          return capi_cuda_fail(e, "alpha op");
+        op = w;
+        ldo = ldw;
+      } else if ((e = launch_scale(rows, cols, w, ldo, alpha, st)) != cudaSuccess) {  // transposed copy: in place
+        return capi_cuda_fail(e, "alpha op");
+      }
+    }
+    ep = Epilogue{};  // the my_dgemm contract
+  }
   e = dispatch(m, n, k, opA, lda_op, opB, ldb_op, C, ldc, st, flags & ~MY_DGEMM_DEVICE_PTRS, ep);
   if (wa) cudaFreeAsync(wa, st);
   if (wb) cudaFreeAsync(wb, st);
@@ -155,7 +205,8 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
   if (!C) return capi_fail(-12, "C is NULL");
 
   if (flags & MY_DGEMM_DEVICE_PTRS)
-    return blas_device(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, flags, (cudaStream_t)stream);
+    return blas_device(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, flags, (cudaStream_t)stream,
+                       true);
 
   // Host operands: stage through stream-ordered device buffers (pitched
   // copies never touch padding rows), run on the device, copy C back.
@@ -184,7 +235,7 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
                                               cudaMemcpyHostToDevice, st)) != cudaSuccess)
       break;
     status = blas_device(transa, transb, m, n, k, alpha, dA, (int)dlda, dB, (int)dldb, beta, dC, (int)dldc,
-                         flags | MY_DGEMM_DEVICE_PTRS, st);
+                         flags | MY_DGEMM_DEVICE_PTRS, st, true);
     if (status != 0) break;
     if ((e = cudaMemcpy2DAsync(C, (size_t)ldc * 8, dC, dldc * 8, (size_t)m * 8, n, cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)

@@ -31,7 +31,7 @@
 namespace myd {
 
 int blas_device(char ta, char tb, int m, int n, int k, double alpha, const double *A, int lda, const double *B,
-                int ldb, double beta, double *C, int ldc, unsigned flags, cudaStream_t st);
+                int ldb, double beta, double *C, int ldc, unsigned flags, cudaStream_t st, bool fold);
 int capi_fail(int status, const std::string &msg);
 int capi_ok();
 int capi_cuda_fail(cudaError_t e, const char *where);
@@ -204,9 +204,9 @@ int update(const Tri &t, int64_t i0, int nb, int64_t p0, int64_t p1, int64_t m, 
   if (kk <= 0 || nb <= 0) return capi_ok();
   if (t.left)
     return blas_device(t.ta(), 'N', nb, (int)n, kk, s, t.blk(i0, p0), (int)t.lda, t.B + p0, (int)t.ldb, 1.0,
-                       t.B + i0, (int)t.ldb, t.flags, t.st);
+                       t.B + i0, (int)t.ldb, t.flags, t.st, false);
   return blas_device('N', t.ta(), (int)m, nb, kk, s, t.B + p0 * t.ldb, (int)t.ldb, t.blk(p0, i0), (int)t.lda, 1.0,
-                     t.B + i0 * t.ldb, (int)t.ldb, t.flags, t.st);
+                     t.B + i0 * t.ldb, (int)t.ldb, t.flags, t.st, false);
 }
 
 // Blocked triangular multiply / solve over [lo_, hi_) of the triangle's
@@ -337,7 +337,7 @@ extern "C" int my_dsyrk(char uplo, char trans, int n, int k, double alpha, const
     const int64_t r0 = lower ? j0 + nb : 0, r1 = lower ? n : j0;
     if (r1 > r0)
       s = blas_device(ta, tb, (int)(r1 - r0), nb, k, alpha, rows(r0), lda, rows(j0), lda, beta, C + j0 * ldc + r0,
-                      ldc, gf, st);
+                      ldc, gf, st, true);  // one large panel: the BLAS order pays
     if (s != 0) break;
     // diagonal block: W = op(A)_j op(A)_j^T from zero, merged into the triangle
     if (alpha == 0.0 || k == 0) {
@@ -345,7 +345,7 @@ extern "C" int my_dsyrk(char uplo, char trans, int n, int k, double alpha, const
         s = capi_cuda_fail(e, "memset");
         break;
       }
-    } else if ((s = blas_device(ta, tb, nb, nb, k, 1.0, rows(j0), lda, rows(j0), lda, 0.0, W, nb, gf, st)) != 0) {
+    } else if ((s = blas_device(ta, tb, nb, nb, k, 1.0, rows(j0), lda, rows(j0), lda, 0.0, W, nb, gf, st, false)) != 0) {
       break;
     }
     syrk_merge_kernel<<<dim3((unsigned)((nb + 255) / 256), (unsigned)nb), 256, 0, st>>>(

@@ -33,7 +33,7 @@ for n in sizes:
     C = torch.rand(n, n, dtype=torch.float64, device="cuda")
     # column-major views: a torch row-major (n, n) tensor is the transpose; fine for timing
     f3 = 1.0 * n ** 3
-    ms = timed(lambda: engine.dsyrk("L", "N", n, n, 1.0, A, n, 1.0, C, n))
+    ms = timed(lambda: engine.dsyrk("L", "N", n, n, -1.0, A, n, 1.0, C, n))
     msg = timed(lambda: torch.mm(A, A.t()))
     print(f"dsyrk  n={n}: {ms:8.3f} ms  {f3 / ms / 1e9:6.2f} TF/s (n^2 k) | cuBLAS full A A^T {msg:8.3f} ms", flush=True)
     Bw = B.clone()
