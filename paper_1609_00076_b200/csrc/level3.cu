@@ -13,7 +13,8 @@
 // * DTRMM / DTRSM: B := alpha op(A) B, B := alpha B op(A) and their solves.
 //   The four side x effective-triangle cases are ordered so that each block
 //   row / column is finished from operands not yet overwritten; blocks of 512
-//   recurse into blocks of 128 and 32, whose diagonal part runs in
+//   recurse into blocks of 128 and 32 (trmm: one dgemm on a dense copy of
+//   each 512 diagonal block instead), whose diagonal part runs in
 //   tri_diag_kernel (one thread per vector, the 32x32 triangle staged in
 //   shared memory, the vector in registers) and the rest in dgemm calls (beta = 1, alpha = +-1).
 //
@@ -160,6 +161,30 @@ __global__ void __launch_bounds__(128) tri_diag_kernel(int nb, int64_t nv, const
     if (r < nb) xv[r * xs_e] = v[r];
 }
 
+// T (nb x nb, ld nb) := the dense op(A) diagonal block: the effective
+// triangle of op(A)(i0.., i0..), zeros elsewhere, ones on the diagonal when unit.
+__global__ void dense_tri_kernel(int nb, const double *__restrict__ A, int64_t lda, bool opt, bool elow, bool unit,
+                                 double *__restrict__ T) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)nb * nb;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nb), c = (int)(e / nb);
+    double v = 0.0;
+    if (r == c)
+      v = unit ? 1.0 : A[(int64_t)c * lda + r];
+    else if (elow ? r > c : r < c)
+      v = opt ? A[(int64_t)r * lda + c] : A[(int64_t)c * lda + r];
+    T[e] = v;
+  }
+}
+
+// dst (rows x cols) := src
+__global__ void copy_kernel(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
+                            double *__restrict__ dst, int64_t ldd) {
+  for (int64_t j = blockIdx.y; j < cols; j += gridDim.y)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x)
+      dst[j * ldd + i] = src[j * lds + i];
+}
+
 // The triangular operation in canonical form: op(A) is effectively lower
 // (`elow`) or upper; `opt`: op(A)(r, c) = A(c, r).  B is m x n.
 struct Tri {
@@ -170,6 +195,7 @@ struct Tri {
   int64_t ldb;
   unsigned flags;
   cudaStream_t st;
+  double *T = nullptr, *W = nullptr;  // multiply: dense diagonal block and its product (dense_block)
   // pointer to op(A)(r0.., c0..) and the transa to use for that block in dgemm
   const double *blk(int64_t r0, int64_t c0) const { return opt ? A + r0 * lda + c0 : A + c0 * lda + r0; }
   char ta() const { return opt ? 'T' : 'N'; }
@@ -209,6 +235,31 @@ int update(const Tri &t, int64_t i0, int nb, int64_t p0, int64_t p1, int64_t m, 
                      t.B + i0 * t.ldb, (int)t.ldb, t.flags, t.st, false);
 }
 
+// Multiply of an outer diagonal block as one dgemm: T := dense op(A)(i, i),
+// W := T B_i (left) or B_i T (right) from zero, B_i := W.  Twice the block's
+// triangle flops, but one full-width dgemm instead of the 128 / 32 recursion
+// (whose small launches dominated: profiles/level3_r01.log).
+int dense_block(const Tri &t, int64_t i0, int nb, int64_t m, int64_t n) {
+  cudaError_t e;
+  const int64_t cnt = (int64_t)nb * nb;
+  dense_tri_kernel<<<(unsigned)std::min<int64_t>((cnt + 255) / 256, 1024), 256, 0, t.st>>>(
+      nb, t.blk(i0, i0), t.lda, t.opt, t.elow, t.unit, t.T);
+  count_launch();
+  if ((e = cudaGetLastError()) != cudaSuccess) return capi_cuda_fail(e, "dense triangle");
+  const int64_t rows = t.left ? nb : m, cols = t.left ? n : nb, ldw = (rows + 1) & ~1LL;
+  double *bi = t.left ? t.B + i0 : t.B + i0 * t.ldb;
+  int s = t.left ? blas_device('N', 'N', nb, (int)n, nb, 1.0, t.T, nb, bi, (int)t.ldb, 0.0, t.W, (int)ldw, t.flags,
+                               t.st, false)
+                 : blas_device('N', 'N', (int)m, nb, nb, 1.0, bi, (int)t.ldb, t.T, nb, 0.0, t.W, (int)ldw, t.flags,
+                               t.st, false);
+  if (s != 0) return s;
+  copy_kernel<<<dim3((unsigned)std::min<int64_t>((rows + 255) / 256, 64), (unsigned)std::min<int64_t>(cols, 65535)),
+                256, 0, t.st>>>(rows, cols, t.W, ldw, bi, t.ldb);
+  count_launch();
+  e = cudaGetLastError();
+  return e == cudaSuccess ? capi_ok() : capi_cuda_fail(e, "copy back");
+}
+
 // Blocked triangular multiply / solve over [lo_, hi_) of the triangle's
 // dimension with block size bs (outer blocks of 512, then 128, then TB
 // inside each diagonal block), left-looking: block i is finished from all of
@@ -235,7 +286,8 @@ int tri_range(const Tri &t, int64_t lo_, int64_t hi_, int bs, int64_t m, int64_t
       s = bs > TB ? tri_range(t, i0, i0 + nb, inner_bs(bs), m, n) : diag(t, i0, nb, m, n);
       if (s != 0) return s;
     } else {  // B_i := diag B_i + sum_p ... B_p (B_p still original)
-      s = bs > TB ? tri_range(t, i0, i0 + nb, inner_bs(bs), m, n) : diag(t, i0, nb, m, n);
+      s = t.T && bs >= 256 ? dense_block(t, i0, nb, m, n)
+                           : (bs > TB ? tri_range(t, i0, i0 + nb, inner_bs(bs), m, n) : diag(t, i0, nb, m, n));
       if (s != 0) return s;
       if ((s = update(t, i0, nb, p0, p1, m, n, 1.0)) != 0) return s;
     }
@@ -287,8 +339,17 @@ int tri(bool solve, char side, char uplo, char transa, char diagc, int m, int n,
   int s;
   if (alpha != 1.0 && (s = scale(m, n, B, ldb, alpha, st)) != 0) return s;
   Tri t{left, lo(uplo) != tr(transa), tr(transa), diagc == 'U' || diagc == 'u', solve, A, lda, B, ldb,
-        flags & MY_DGEMM_FORCE_TILED, st};
-  s = tri_range(t, 0, na, na > TB ? std::min(blocks().outer, ((na + TB - 1) / TB) * TB) : TB, m, n);
+        flags & MY_DGEMM_FORCE_TILED, st, nullptr, nullptr};
+  const int bs0 = na > TB ? std::min(blocks().outer, ((na + TB - 1) / TB) * TB) : TB;
+  if (!solve && bs0 >= 256) {  // dense diagonal-block multiply: T and W workspace
+    const int64_t rows = left ? bs0 : m, cols = left ? n : bs0;
+    cudaError_t e = cudaMallocAsync((void **)&t.T, (size_t)bs0 * bs0 * 8, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&t.W, (size_t)((rows + 1) & ~1LL) * cols * 8, st);
+    if (e != cudaSuccess) return capi_cuda_fail(e, "cudaMallocAsync(trmm block)");
+  }
+  s = tri_range(t, 0, na, bs0, m, n);
+  if (t.T) cudaFreeAsync(t.T, st);
+  if (t.W) cudaFreeAsync(t.W, st);
   return s;
 }
 
