@@ -50,6 +50,9 @@ extern "C" {
 #define MY_DGEMM_FORCE_ROWS16 0x80u  /* run every tile as eight 16x128 units (tests) */
 #define MY_DGEMM_FORCE_STREAMK 0x800u /* stream-K schedule (tests): of full tiles, or with STRIPS2 / STRIPS4 /
                                           UNITS8 of those units, when there is at least one per SM */
+#define MY_DGEMM_BLAS_EPILOGUE 0x1000u /* my_dgemm_blas (tests): apply alpha / beta in the kernel epilogue
+                                          instead of the reference-BLAS order (C := beta C, alpha folded
+                                          into an operand, then the contract) that large tiled calls use */
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The
@@ -171,6 +174,19 @@ MY_DGEMM_API uint64_t my_dgemm_operand_seed(uint64_t seed, uint64_t role, int64_
  */
 MY_DGEMM_API int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
                           double tol, double *out_max, int64_t *out_first_bad, void *stream);
+
+/*
+ * The same scan plus the offender's pair (X and Y at the first bad element),
+ * i.e. the reference's DiffReport (matrix.py:90-107: max_abs_diff,
+ * first_bad_i/j, value_got, value_expected) from which its
+ * "C[ i ][ j ] != C_ref, %E, %E" line is formed (bench.py:84-86,150-156).
+ * out_got / out_want are left untouched when there is no offender.
+ * Offender rule as the reference: strict |X - Y| > tol, so a NaN difference
+ * is not an offender but makes out_max NaN.
+ */
+MY_DGEMM_API int my_dgemm_diff_report(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y,
+                                      int64_t ldy, double tol, double *out_max, int64_t *out_first_bad,
+                                      double *out_got, double *out_want, void *stream);
 
 /*
  * CTA-plan autotuner (the GPU analogue of the reference's grid tuner,

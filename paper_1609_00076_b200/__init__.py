@@ -20,7 +20,12 @@ from .engine import (  # noqa: F401
     fill_random_device,
     gemm_b200,
     kernel_launches,
+    DiffReport,
+    VerificationError,
+    diff_report_device,
+    failure_line,
     max_abs_diff_device,
+    verify_device,
     my_dgemm,
     operand_seed,
     register,

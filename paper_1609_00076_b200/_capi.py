@@ -24,6 +24,7 @@ FORCE_STRIPS4 = 0x20
 FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
 FORCE_STREAMK = 0x800
+BLAS_EPILOGUE = 0x1000
 IPC_HANDLE_BYTES = 64
 PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT, PATH_ROWS_DMMA = range(7)
 
@@ -55,6 +56,8 @@ SIGNATURES = {
     "my_dgemm_operand_seed": (_U64, [_U64, _U64, _I64, _I64, _I64]),
     "my_dgemm_max_abs_diff": (_I, [_I64, _I64, _P, _I64, _P, _I64, _D, ctypes.POINTER(_D),
                                    ctypes.POINTER(_I64), _P]),
+    "my_dgemm_diff_report": (_I, [_I64, _I64, _P, _I64, _P, _I64, _D, ctypes.POINTER(_D),
+                                  ctypes.POINTER(_I64), ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
     "my_dgemm_tune": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_D)]),
     "my_dgemm_tune_clear": (None, []),
     "my_dgemm_set_max_ctas": (_I, [_I]),

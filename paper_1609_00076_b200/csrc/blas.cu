@@ -112,7 +112,16 @@ int blas_device(char ta, char tb, int m, int n, int k, double alpha, const doubl
   const bool tA = is_trans(ta), tB = is_trans(tb);
   if (tA || tB) keep_pool_memory();
   const int64_t ldA = ((int64_t)m + 1) & ~1LL, ldB = ((int64_t)k + 1) & ~1LL;
-  double *wa = nullptr, *wb = nullptr;
+  // workspace freed (stream-ordered) on every return path
+  struct Scratch {
+    double *p[2] = {nullptr, nullptr};
+    cudaStream_t st;
+    ~Scratch() {
+      for (double *q : p)
+        if (q) cudaFreeAsync(q, st);
+    }
+  } scratch{{nullptr, nullptr}, st};
+  double *&wa = scratch.p[0], *&wb = scratch.p[1];
   const double *opA = A, *opB = B;
   int64_t lda_op = lda, ldb_op = ldb;
   if (tA) {  // A stored k x m; op(A) = A^T (m x k)
@@ -157,8 +166,6 @@ int blas_device(char ta, char tb, int m, int n, int k, double alpha, const doubl
     ep = Epilogue{};  // the my_dgemm contract
   }
   e = dispatch(m, n, k, opA, lda_op, opB, ldb_op, C, ldc, st, flags & ~MY_DGEMM_DEVICE_PTRS, ep);
-  if (wa) cudaFreeAsync(wa, st);
-  if (wb) cudaFreeAsync(wb, st);
   return e == cudaSuccess ? capi_ok() : capi_cuda_fail(e, "kernel launch");
 }
 
@@ -191,8 +198,11 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
   }
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
-                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_FORCE_STREAMK | MY_DGEMM_PATH_MASK;
+                         MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_FORCE_STREAMK | MY_DGEMM_PATH_MASK |
+                         MY_DGEMM_BLAS_EPILOGUE;
   if (flags & ~known) return capi_fail(-14, "unknown flag bits");
+  const bool fold = !(flags & MY_DGEMM_BLAS_EPILOGUE);
+  flags &= ~MY_DGEMM_BLAS_EPILOGUE;
   if (m > 0 && n > 0 && !path_fits(m, n, flags))
     return capi_fail(-14, "MY_DGEMM_FORCE_PATH does not suit the shape");
   if ((flags & MY_DGEMM_EXACT) && !(alpha == 1.0 && beta == 1.0))
@@ -206,7 +216,7 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
 
   if (flags & MY_DGEMM_DEVICE_PTRS)
     return blas_device(transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, flags, (cudaStream_t)stream,
-                       true);
+                       fold);
 
   // Host operands: stage through stream-ordered device buffers (pitched
   // copies never touch padding rows), run on the device, copy C back.
@@ -235,7 +245,7 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
                                               cudaMemcpyHostToDevice, st)) != cudaSuccess)
       break;
     status = blas_device(transa, transb, m, n, k, alpha, dA, (int)dlda, dB, (int)dldb, beta, dC, (int)dldc,
-                         flags | MY_DGEMM_DEVICE_PTRS, st, true);
+                         flags | MY_DGEMM_DEVICE_PTRS, st, fold);
     if (status != 0) break;
     if ((e = cudaMemcpy2DAsync(C, (size_t)ldc * 8, dC, dldc * 8, (size_t)m * 8, n, cudaMemcpyDeviceToHost, st)) !=
         cudaSuccess)

@@ -310,8 +310,8 @@ uint64_t my_dgemm_operand_seed(uint64_t seed, uint64_t role, int64_t m, int64_t 
   return h;
 }
 
-int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
-                          double tol, double *out_max, int64_t *out_first_bad, void *stream) {
+int my_dgemm_diff_report(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy, double tol,
+                         double *out_max, int64_t *out_first_bad, double *out_got, double *out_want, void *stream) {
   if (m < 1) return fail(-1, "matrix dims must be positive");
   if (n < 1) return fail(-2, "matrix dims must be positive");
   if (!X) return fail(-3, "X is NULL");
@@ -332,9 +332,25 @@ int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, co
   if (e != cudaSuccess) return cuda_fail(e, "max_abs_diff");
   double mx;
   memcpy(&mx, &h[0], 8);
+  const int64_t first = (h[1] == ~0ULL) ? -1 : (int64_t)h[1];
   if (out_max) *out_max = mx;
-  if (out_first_bad) *out_first_bad = (h[1] == ~0ULL) ? -1 : (int64_t)h[1];
+  if (out_first_bad) *out_first_bad = first;
+  if (first >= 0 && (out_got || out_want)) {  // the offender's pair, for the reference's failure line
+    const int64_t j = first / m, i = first % m;
+    double g = 0.0, w = 0.0;
+    e = cudaMemcpyAsync(&g, X + j * ldx + i, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&w, Y + j * ldy + i, 8, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "max_abs_diff offender");
+    if (out_got) *out_got = g;
+    if (out_want) *out_want = w;
+  }
   return ok();
+}
+
+int my_dgemm_max_abs_diff(int64_t m, int64_t n, const double *X, int64_t ldx, const double *Y, int64_t ldy,
+                          double tol, double *out_max, int64_t *out_first_bad, void *stream) {
+  return my_dgemm_diff_report(m, n, X, ldx, Y, ldy, tol, out_max, out_first_bad, nullptr, nullptr, stream);
 }
 
 const char *my_dgemm_last_error(void) { return t_error.c_str(); }

@@ -174,9 +174,12 @@ cudaError_t launch_copy2d(int64_t rows, int64_t cols, const double *src, int64_t
 
 // ---------------------------------------------------------------------------
 // max_abs_diff (matrix.py:210-232): max |X-Y| over the valid region and the
-// first flat index t = j*m + i with |X-Y| > tol (NaN counts as bad).  Max and
-// min are order-independent, so atomics keep the answer deterministic.
-// Non-negative doubles order like their bit patterns, NaN above +inf.
+// first flat index t = j*m + i with |X-Y| > tol -- strict, as the reference's
+// `flat > tol` (matrix.py:226): a NaN difference is not an offender there
+// either, but it does make the max NaN (numpy's max propagates it), and a
+// caller's `max <= bound` check then fails.  Max and min are
+// order-independent, so atomics keep the answer deterministic.  Non-negative
+// doubles order like their bit patterns, NaN above +inf.
 // ---------------------------------------------------------------------------
 __global__ void max_abs_diff_kernel(int64_t m, int64_t n, const double *__restrict__ X, int64_t ldx,
                                     const double *__restrict__ Y, int64_t ldy, double tol,
@@ -187,7 +190,7 @@ __global__ void max_abs_diff_kernel(int64_t m, int64_t n, const double *__restri
       const double d = fabs(X[j * ldx + i] - Y[j * ldy + i]);
       const unsigned long long bits = (unsigned long long)__double_as_longlong(d);
       local_max = bits > local_max ? bits : local_max;
-      if (!(d <= tol)) {
+      if (d > tol) {
         const unsigned long long t = (unsigned long long)(j * m + i);
         local_first = t < local_first ? t : local_first;
       }

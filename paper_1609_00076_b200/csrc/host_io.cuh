@@ -14,6 +14,7 @@
 #include <cstring>
 #include <deque>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -32,28 +33,43 @@ class CopyPool {
   }
   // Run fn(i) for i in [0, n) on the pool and the calling thread; blocks.
   // One job at a time (concurrent callers -- the per-device threads of the
-  // multi-device path -- take turns).
+  // multi-device path -- take turns).  Each job's state (index counter, done
+  // count) lives in its own shared Job, which a worker snapshots under the
+  // lock: a worker that wakes late for a finished job only ever sees that
+  // job's exhausted counter, never the next job's indices, and never calls a
+  // function whose caller has returned.
   void parallel_for(int n, const std::function<void(int)> &fn) {
     if (n <= 1 || workers_.empty()) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
     }
     std::lock_guard<std::mutex> run(run_mu_);
-    std::unique_lock<std::mutex> lk(mu_);
-    job_ = &fn;
-    total_ = n;
-    next_.store(0);
-    done_ = 0;
-    ++gen_;
+    auto job = std::make_shared<Job>(&fn, n);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = job;
+      ++gen_;
+    }
     cv_.notify_all();
-    lk.unlock();
-    work();
-    lk.lock();
-    done_cv_.wait(lk, [&] { return done_ == total_; });
-    job_ = nullptr;
+    work(*job);
+    {
+      std::unique_lock<std::mutex> lk(job->mu);
+      job->cv.wait(lk, [&] { return job->done == job->total; });
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    job_.reset();
   }
 
  private:
+  struct Job {
+    Job(const std::function<void(int)> *f, int n) : fn(f), total(n) {}
+    const std::function<void(int)> *fn;
+    const int total;
+    std::atomic<int> next{0};
+    int done = 0;  // guarded by mu
+    std::mutex mu;
+    std::condition_variable cv;
+  };
   CopyPool() {
     int want = 8;
     if (const char *s = getenv("MY_DGEMM_HOST_THREADS")) want = std::max(1, atoi(s));
@@ -72,33 +88,33 @@ class CopyPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
-      if (stop_) return;
-      seen = gen_;
-      lk.unlock();
-      work();
+      std::shared_ptr<Job> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && job_); });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      work(*job);
     }
   }
-  void work() {
-    const std::function<void(int)> *fn = job_;
+  static void work(Job &job) {
     int did = 0;
-    for (int i = next_.fetch_add(1); i < total_; i = next_.fetch_add(1)) {
-      (*fn)(i);
+    for (int i = job.next.fetch_add(1); i < job.total; i = job.next.fetch_add(1)) {
+      (*job.fn)(i);
       ++did;
     }
     if (did) {
-      std::lock_guard<std::mutex> lk(mu_);
-      done_ += did;
-      if (done_ == total_) done_cv_.notify_all();
+      std::lock_guard<std::mutex> lk(job.mu);
+      job.done += did;
+      if (job.done == job.total) job.cv.notify_all();
     }
   }
   std::vector<std::thread> workers_;
   std::mutex run_mu_, mu_;
-  std::condition_variable cv_, done_cv_;
-  const std::function<void(int)> *job_ = nullptr;
-  std::atomic<int> next_{0};
-  int total_ = 0, done_ = 0;
+  std::condition_variable cv_;
+  std::shared_ptr<Job> job_;
   uint64_t gen_ = 0;
   bool stop_ = false;
 };

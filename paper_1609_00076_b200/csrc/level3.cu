@@ -177,6 +177,47 @@ __global__ void dense_tri_kernel(int nb, const double *__restrict__ A, int64_t l
   }
 }
 
+// After dense_block's W := T B_i (left) or B_i T (right): every vector of B_i
+// holding an Inf or NaN has its W vector recomputed from the triangle only,
+// so the zeros dense_tri_kernel wrote outside the triangle never meet a
+// non-finite B value (0 * Inf would turn a finite or infinite result into
+// NaN; reference BLAS reads the triangle only).  One warp per column (left:
+// columns of B_i are the vectors) or one thread per row (right: rows are the
+// vectors, read across threads so the scan is coalesced).  For finite B the
+// kernel is a read-only scan of B_i.
+__global__ void trmm_nonfinite_fix_kernel(bool left, bool elow, int nb, int64_t nv, const double *__restrict__ T,
+                                          const double *__restrict__ bi, int64_t ldb, double *__restrict__ W,
+                                          int64_t ldw) {
+  if (left) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nv;
+         j += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+      const double *b = bi + j * ldb;
+      bool bad = false;
+      for (int c = lane; c < nb; c += 32) bad |= !isfinite(b[c]);
+      if (!__any_sync(0xffffffffu, bad)) continue;
+      for (int r = lane; r < nb; r += 32) {
+        double s = 0.0;
+        const int c0 = elow ? 0 : r, c1 = elow ? r + 1 : nb;
+        for (int c = c0; c < c1; ++c) s += T[(int64_t)c * nb + r] * b[c];
+        W[j * ldw + r] = s;
+      }
+    }
+  } else {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nv; r += (int64_t)gridDim.x * blockDim.x) {
+      bool bad = false;
+      for (int c = 0; c < nb; ++c) bad |= !isfinite(bi[(int64_t)c * ldb + r]);
+      if (!bad) continue;
+      for (int cc = 0; cc < nb; ++cc) {  // W(r, cc) = sum over the triangle's column cc of B_i(r, c) T(c, cc)
+        double s = 0.0;
+        const int c0 = elow ? cc : 0, c1 = elow ? nb : cc + 1;
+        for (int c = c0; c < c1; ++c) s += bi[(int64_t)c * ldb + r] * T[(int64_t)cc * nb + c];
+        W[cc * ldw + r] = s;
+      }
+    }
+  }
+}
+
 // dst (rows x cols) := src
 __global__ void copy_kernel(int64_t rows, int64_t cols, const double *__restrict__ src, int64_t lds,
                             double *__restrict__ dst, int64_t ldd) {
@@ -253,6 +294,14 @@ int dense_block(const Tri &t, int64_t i0, int nb, int64_t m, int64_t n) {
                  : blas_device('N', 'N', (int)m, nb, nb, 1.0, bi, (int)t.ldb, t.T, nb, 0.0, t.W, (int)ldw, t.flags,
                                t.st, false);
   if (s != 0) return s;
+  {
+    const int64_t nv = t.left ? n : m;
+    const int64_t threads = t.left ? nv * 32 : nv;
+    trmm_nonfinite_fix_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((threads + 255) / 256, 4096)), 256,
+                                0, t.st>>>(t.left, t.elow, nb, nv, t.T, bi, t.ldb, t.W, ldw);
+    count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return capi_cuda_fail(e, "trmm non-finite fix");
+  }
   copy_kernel<<<dim3((unsigned)std::min<int64_t>((rows + 255) / 256, 64), (unsigned)std::min<int64_t>(cols, 65535)),
                 256, 0, t.st>>>(rows, cols, t.W, ldw, bi, t.ldb);
   count_launch();
@@ -345,7 +394,10 @@ int tri(bool solve, char side, char uplo, char transa, char diagc, int m, int n,
     const int64_t rows = left ? bs0 : m, cols = left ? n : bs0;
     cudaError_t e = cudaMallocAsync((void **)&t.T, (size_t)bs0 * bs0 * 8, st);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&t.W, (size_t)((rows + 1) & ~1LL) * cols * 8, st);
-    if (e != cudaSuccess) return capi_cuda_fail(e, "cudaMallocAsync(trmm block)");
+    if (e != cudaSuccess) {
+      if (t.T) cudaFreeAsync(t.T, st);
+      return capi_cuda_fail(e, "cudaMallocAsync(trmm block)");
+    }
   }
   s = tri_range(t, 0, na, bs0, m, n);
   if (t.T) cudaFreeAsync(t.T, st);

@@ -51,6 +51,11 @@ __all__ = [
     "fill_random_device",
     "operand_seed",
     "max_abs_diff_device",
+    "DiffReport",
+    "diff_report_device",
+    "failure_line",
+    "VerificationError",
+    "verify_device",
     "kernel_launches",
     "dgemm",
     "tune",
@@ -278,6 +283,77 @@ def max_abs_diff_device(m: int, n: int, x_ptr: int, ldx: int, y_ptr: int, ldy: i
     return mx.value, i, j
 
 
+class DiffReport:
+    """matrix.py:90-107 `DiffReport`: the largest |got - want| and, iff some
+    difference exceeds the tolerance, the first offender in column-major scan
+    order with its two values."""
+
+    __slots__ = ("max_abs_diff", "first_bad_i", "first_bad_j", "value_got", "value_expected")
+
+    def __init__(self, max_abs_diff, first_bad_i=None, first_bad_j=None, value_got=None, value_expected=None):
+        self.max_abs_diff = max_abs_diff
+        self.first_bad_i = first_bad_i
+        self.first_bad_j = first_bad_j
+        self.value_got = value_got
+        self.value_expected = value_expected
+
+    @property
+    def clean(self) -> bool:
+        return self.first_bad_i is None
+
+    def __repr__(self) -> str:
+        return (f"DiffReport(max_abs_diff={self.max_abs_diff!r}, first_bad_i={self.first_bad_i!r}, "
+                f"first_bad_j={self.first_bad_j!r}, value_got={self.value_got!r}, "
+                f"value_expected={self.value_expected!r})")
+
+
+def failure_line(i: int, j: int, got: float, want: float) -> str:
+    """bench.py:84-86: the mismatch diagnostic in the classic test-driver form."""
+    return f"C[ {i} ][ {j} ] != C_ref, {got:.6E}, {want:.6E}"
+
+
+class VerificationError(RuntimeError):
+    """bench.py:74-81: a result outside tolerance of the oracle; `diagnostic`
+    is the failure line."""
+
+    def __init__(self, diagnostic: str, m=None, n=None, k=None, algorithm=None):
+        super().__init__(diagnostic)
+        self.diagnostic = diagnostic
+        self.m, self.n, self.k = m, n, k
+        self.algorithm = algorithm
+
+
+def diff_report_device(m: int, n: int, got_ptr: int, ld_got: int, want_ptr: int, ld_want: int,
+                       tol: float = 0.0, stream: int = 0) -> DiffReport:
+    """matrix.py:210-232 `max_abs_diff` on device-resident matrices: the
+    reference's DiffReport (strict > tol offender rule, column-major first
+    offender, NaN max when a difference is NaN)."""
+    lib = _capi.load()
+    mx, first, got, want = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+    _capi.check(lib.my_dgemm_diff_report(m, n, got_ptr, ld_got, want_ptr, ld_want, tol, ctypes.byref(mx),
+                                         ctypes.byref(first), ctypes.byref(got), ctypes.byref(want),
+                                         ctypes.c_void_p(stream)))
+    if first.value < 0:
+        return DiffReport(mx.value)
+    j, i = divmod(first.value, m)
+    return DiffReport(mx.value, i, j, got.value, want.value)
+
+
+def verify_device(m: int, n: int, k: int, got_ptr: int, ld_got: int, want_ptr: int, ld_want: int, tol: float,
+                  algorithm: str = "b200", stream: int = 0) -> DiffReport:
+    """run_sweep's check (bench.py:140-156) on the device: raise
+    VerificationError carrying the reference's failure line at the first
+    offender; also raise when the max difference is NaN (which the strict
+    offender rule alone would let through)."""
+    rep = diff_report_device(m, n, got_ptr, ld_got, want_ptr, ld_want, tol, stream)
+    if not rep.clean:
+        raise VerificationError(failure_line(rep.first_bad_i, rep.first_bad_j, rep.value_got, rep.value_expected),
+                                m=m, n=n, k=k, algorithm=algorithm)
+    if rep.max_abs_diff != rep.max_abs_diff:
+        raise VerificationError(f"max |C - C_ref| is NaN over {m}x{n}", m=m, n=n, k=k, algorithm=algorithm)
+    return rep
+
+
 def path(m: int, n: int, exact: bool = False) -> int:
     """Kernel family of an (m, n) call (my_dgemm_path): _capi.PATH_TILED or
     one of the bandwidth kernels.  Sharded drivers force the tiled kernel on
@@ -302,15 +378,16 @@ def kernel_launches() -> int:
 
 
 def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A, lda: int, B, ldb: int,
-          beta: float, C, ldc: int, exact: bool = False, stream: int | None = None):
+          beta: float, C, ldc: int, exact: bool = False, stream: int | None = None, epilogue: bool = False):
     """BLAS dgemm: C := alpha op(A) op(B) + beta C.
 
     Host numpy buffers (synchronous) or torch CUDA tensors (asynchronous on
     `stream`, default torch's current stream).  Argument errors raise
-    ValueError naming the BLAS parameter.
+    ValueError naming the BLAS parameter.  `epilogue` (tests) forces alpha /
+    beta into the kernel epilogue instead of the reference-BLAS order.
     """
     lib = _capi.load()
-    flags = _flags(exact)
+    flags = _flags(exact) | (_capi.BLAS_EPILOGUE if epilogue else 0)
     dev = _is_device(C)
     if dev:
         if stream is None:

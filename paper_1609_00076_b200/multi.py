@@ -235,3 +235,90 @@ class ShardedDgemm:
             for w in works:
                 w.wait()
         return C_local
+
+    # -- one step from host buffers (the end-to-end measurement) ----------
+    def step_host(self, hA, A, lda: int, hB_local, B_local, ldb: int, hC_local, C_local, ldc: int):
+        """The same step with the operands in (pinned) host memory: every
+        rank uploads its B / C panel, the root uploads A chunk by chunk and
+        each chunk's broadcast starts as soon as it has landed, the GEMM
+        follows the configured schedule, and the C panel comes back to the
+        host.  Host-synchronous.  hA is read on the root only; hB_local /
+        hC_local are this rank's panels (ldb / ldc pitched like the device
+        panels).  The copy-engine chain exchange uploads all of A first."""
+        p = self.plan
+        nloc = p.local(self.rank)[1] - p.local(self.rank)[0]
+        cuda = A.is_cuda
+        root = self.rank == p.root
+        spans = [a_span(lda, p.m, p0, p1) for (p0, p1) in p.chunks]
+        nb, nc = (nloc - 1) * ldb + p.k if nloc else 0, (nloc - 1) * ldc + p.m if nloc else 0
+        if cuda:
+            import torch
+
+            cs = self._stream()
+            up = self._upload_stream(A.device)
+            up.wait_stream(cs)  # the buffers are free once the previous step's work is done
+            ctx = torch.cuda.stream(up)
+        else:
+            import contextlib
+
+            ctx = contextlib.nullcontext()
+        works, landed = [], []
+        with ctx:
+            if nloc:
+                B_local[:nb].copy_(hB_local[:nb], non_blocking=True)
+                C_local[:nc].copy_(hC_local[:nc], non_blocking=True)
+            panels = self._record(up) if cuda else None
+            for lo, hi in spans:
+                if root:
+                    A[lo:hi].copy_(hA[lo:hi], non_blocking=True)
+                    landed.append(self._record(up) if cuda else None)
+                if p.world > 1 and self.chain is None:
+                    works.append(self._broadcast(A[lo:hi], p.root))  # NCCL waits on `up` (the upload)
+        if cuda:
+            cs.wait_event(panels)
+        if self.chain is not None and p.world > 1:
+            for ev in landed:
+                cs.wait_event(ev)
+            self._step_chain(A, lda, B_local, ldb, C_local, ldc)
+        else:
+            def arrived(ci):
+                if root:
+                    if cuda:
+                        cs.wait_event(landed[ci])
+                elif works:
+                    works[ci].wait()
+
+            if self.overlap:
+                for ci, ((p0, p1), (lo, hi)) in enumerate(zip(p.chunks, spans)):
+                    arrived(ci)
+                    if nloc > 0:
+                        self._compute(p.m, nloc, p1 - p0, A[lo:hi], lda, B_local[p0:], ldb, C_local, ldc)
+            else:
+                for ci in range(len(spans)):
+                    arrived(ci)
+                if nloc > 0:
+                    self._compute(p.m, nloc, p.k, A[:spans[-1][1]], lda, B_local, ldb, C_local, ldc)
+            if root and works:
+                for w in works:
+                    w.wait()
+        if nloc:
+            hC_local[:nc].copy_(C_local[:nc], non_blocking=cuda)
+        if cuda:
+            cs.synchronize()
+        return hC_local
+
+    def _upload_stream(self, device):
+        import torch
+
+        if getattr(self, "_up", None) is None:
+            self._up = torch.cuda.Stream(device=device)
+        return self._up
+
+    @staticmethod
+    def _record(stream):
+        import torch
+
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
+

@@ -15,6 +15,13 @@ from oracle/, which the fixtures then pin (tests/test_oracle.py).
 
 Output: tests/golden/golden.json (hashes, sampled values, seeds) and
 tests/golden/small_cases.npz (full C_ref of the small shapes).
+
+    python tests/golden/make_golden.py --parts sampled,kat_large
+
+regenerates only the named parts and merges them into the existing
+golden.json (parts: base = generator/seed/pack pins, kat = full-GEMM hashes
+up to 2048 plus cfg3/cfg4, kat_large = cfg2 2304..8192, sampled = the 64 x 64
+sampled grids of cfg2@8192 and cfg5).
 """
 
 from __future__ import annotations
@@ -77,9 +84,61 @@ def reference_gemm(m, n, k, lda=None, ldb=None, ldc=None):
     return a, b, c
 
 
+def sample_grid(m: int, n: int, tile: int = 128, shards: int = 8, count: int = 64):
+    """64 row and 64 column indices: the first and last elements, every
+    tile-boundary pair (127/128, 255/256, ...) near both ends, the 2-, 4- and
+    8-way jc shard boundaries (split_columns: n/G per rank when 128 | n/G),
+    the middle, and seeded random fill up to `count`."""
+    def pick(size, with_shards):
+        idx = {0, 1, 2, 7, 8, 15, 16, 31, 32, 63, 64, size // 2 - 1, size // 2, size - 2, size - 1}
+        for t in (1, 2, 3, 4):
+            idx.update({t * tile - 1, t * tile, size - t * tile - 1, size - t * tile})
+        if with_shards:
+            for g in range(1, shards):
+                idx.update({g * size // shards - 1, g * size // shards})
+        rng = np.random.default_rng(size * 7919 + (1 if with_shards else 0))
+        while len(idx) < count:
+            idx.add(int(rng.integers(0, size)))
+        return sorted(idx)
+    return pick(m, False), pick(n, True)
+
+
+def sampled_elements(name, m, n, k):
+    """C_ref(i, j) on the sample grid, each element gemm_naive on the 1 x k
+    row of A and the k x 1 column of B plus c_ij (bitwise the full-GEMM
+    element: the per-element order is p-ascending).  A's rows come from
+    random_values over each column p of A (positions p*m .. p*m+m-1)."""
+    rows, cols = sample_grid(m, n)
+    sa, sb, sc = (_operand_seed(SEED, r, m, n, k) for r in (1, 2, 3))
+    ridx = np.asarray(rows)
+    arows = np.empty((len(rows), k))
+    for p in range(k):
+        arows[:, p] = random_values(sa, m, start=p * m)[ridx]
+    vals = []
+    for r, i in enumerate(rows):
+        arow = Matrix(1, k, 1, np.ascontiguousarray(arows[r]))
+        for j in cols:
+            bcol = Matrix(k, 1, k, random_values(sb, k, start=j * k))
+            cij = Matrix(1, 1, 1, random_values(sc, 1, start=j * m + i))
+            vals.append(float(gemm_naive(arow, bcol, cij).data[0]))
+    return {"m": m, "n": n, "k": k, "rows": rows, "cols": cols, "values": vals}
+
+
 def main():
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--parts", default="base,kat,kat_large,sampled")
+    parts = set(ap.parse_args().parts.split(","))
     t0 = time.time()
-    out: dict = {"reference": "gemmforge " + gemmforge.__version__, "seed": SEED}
+    path = os.path.join(HERE, "golden.json")
+    out: dict = {}
+    if parts != {"base", "kat", "kat_large", "sampled"} and os.path.exists(path):
+        with open(path) as f:
+            out = json.load(f)  # merge the regenerated parts into the committed fixtures
+    out.update({"reference": "gemmforge " + gemmforge.__version__, "seed": SEED})
+    if "base" not in parts:
+        return main_parts(out, parts, path, t0)
 
     # -- generator pins (matrix.py:184-207; reference tests/test_matrix.py) --
     out["random_values"] = {
@@ -113,18 +172,26 @@ def main():
         "b_5x7_ld6_seed211_nr3": pack_b(b, 3).buffer.tolist(),
     }
 
+    return main_parts(out, parts, path, t0)
+
+
+def main_parts(out, parts, path, t0):
     # -- full-GEMM known answers (sha256 of the valid region) --
-    kat = {}
+    kat = out.get("kat", {})
     full_small = {}
-    cases = [("cfg1", 512, 512, 512, None)]
-    cases += [(f"cfg2_{s}", s, s, s, None) for s in range(256, 2048 + 1, 256) if s != 512]
-    cases += [
-        ("cfg3a", 4093, 4099, 2047, (4093 + 7, 2047 + 5, 4093 + 3)),
-        ("cfg3b", 1, 8192, 8192, (1 + 7, 8192 + 5, 1 + 3)),
-        ("cfg3c", 8192, 1, 8192, (8192 + 7, 8192 + 5, 8192 + 3)),
-        ("cfg3d", 37, 53, 71, (37 + 7, 71 + 5, 37 + 3)),
-        ("cfg4", 16384, 16384, 256, None),
-    ]
+    cases = []
+    if "kat" in parts:
+        cases += [("cfg1", 512, 512, 512, None)]
+        cases += [(f"cfg2_{s}", s, s, s, None) for s in range(256, 2048 + 1, 256) if s != 512]
+        cases += [
+            ("cfg3a", 4093, 4099, 2047, (4093 + 7, 2047 + 5, 4093 + 3)),
+            ("cfg3b", 1, 8192, 8192, (1 + 7, 8192 + 5, 1 + 3)),
+            ("cfg3c", 8192, 1, 8192, (8192 + 7, 8192 + 5, 8192 + 3)),
+            ("cfg3d", 37, 53, 71, (37 + 7, 71 + 5, 37 + 3)),
+            ("cfg4", 16384, 16384, 256, None),
+        ]
+    if "kat_large" in parts:  # the rest of the cfg2 sweep: every timed size has a bitwise KAT
+        cases += [(f"cfg2_{s}", s, s, s, None) for s in range(2304, 8192 + 1, 256)]
     for name, m, n, k, lds in cases:
         t1 = time.time()
         if lds is None:
@@ -138,6 +205,8 @@ def main():
             full_small[name] = to_array(c)
         print(f"{name}: {time.time() - t1:.1f}s", flush=True)
     out["kat"] = kat
+    if "kat" not in parts:
+        return finish(out, parts, path, t0, full_small)
 
     # -- small problems: registry gate and CLI verify shapes (registry.py:46-51,
     #    127-137; cli.py:66), full C_ref arrays --
@@ -154,28 +223,24 @@ def main():
         a, b, c = make_operands(SEED, m, n, k)
         full_small[f"verify_{m}_{n}_{k}"] = to_array(gemm_naive(a, b, c))
 
-    # -- sampled elements of the big shapes (gemm_naive on a 1 x k row of A and
-    #    a k x 1 column of B plus c_ij: bitwise the full-GEMM element) --
-    sampled = {}
-    for name, (m, n, k) in (("cfg2_8192", (8192, 8192, 8192)), ("cfg5", (32768, 32768, 32768))):
-        rows = [0, 1, 127, 128, m // 2 + 3, m - 2, m - 1]
-        cols = [0, 1, 63, 64, n // 3, n - 1]
-        sa, sb, sc = (_operand_seed(SEED, r, m, n, k) for r in (1, 2, 3))
-        vals = []
-        for i in rows:
-            arow = Matrix(1, k, 1, np.ascontiguousarray(
-                [random_values(sa, 1, start=p * m + i)[0] for p in range(k)]))
-            for j in cols:
-                bcol = Matrix(k, 1, k, random_values(sb, k, start=j * k))
-                cij = Matrix(1, 1, 1, random_values(sc, 1, start=j * m + i))
-                vals.append(float(gemm_naive(arow, bcol, cij).data[0]))
-        sampled[name] = {"m": m, "n": n, "k": k, "rows": rows, "cols": cols, "values": vals}
-        print(f"sampled {name}: done", flush=True)
-    out["sampled"] = sampled
+    return finish(out, parts, path, t0, full_small)
 
-    with open(os.path.join(HERE, "golden.json"), "w") as f:
+
+def finish(out, parts, path, t0, full_small):
+    # -- sampled elements of the big shapes: 64 x 64 grids with tile and
+    #    shard boundaries (SURVEY 8d oracle coverage) --
+    if "sampled" in parts:
+        sampled = out.get("sampled", {})
+        for name, (m, n, k) in (("cfg2_8192", (8192, 8192, 8192)), ("cfg5", (32768, 32768, 32768))):
+            t1 = time.time()
+            sampled[name] = sampled_elements(name, m, n, k)
+            print(f"sampled {name}: {time.time() - t1:.1f}s", flush=True)
+        out["sampled"] = sampled
+
+    with open(path, "w") as f:
         json.dump(out, f, indent=1)
-    np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **full_small)
+    if full_small:
+        np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **full_small)
     print(f"wrote golden fixtures in {time.time() - t0:.1f}s")
 
 

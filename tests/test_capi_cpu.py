@@ -6,6 +6,7 @@ matrix.py:50-53, goto.py:196-204).  No compute is launched here."""
 import ctypes
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -225,3 +226,30 @@ def test_forced_path_must_suit_the_shape(lib):
     p = a.ctypes.data
     assert lib.my_dgemm_ex(4, 4, 4, p, 4, p, 4, p, 4, FP[1], None) == -10
     assert "FORCE_PATH" in lib.my_dgemm_last_error().decode()
+
+
+def test_diagnostics_mirror_the_reference():
+    """engine.failure_line / DiffReport / VerificationError restate
+    bench.py:74-86 and matrix.py:90-107; checked against the reference
+    package itself when oracle/_ref holds it, else against the oracle."""
+    from paper_1609_00076_b200 import engine
+    import oracle
+
+    cases = [(0, 0, 1.0, 2.0), (127, 4096, -3.25e-17, float("inf")), (5, 7, float("nan"), 0.0)]
+    ref_line = oracle.failure_line
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref, "gemmforge")):
+        sys.path.insert(0, ref)
+        try:
+            from gemmforge.bench import VerificationError as RefVE, failure_line as ref_line  # noqa: F811
+            assert issubclass(engine.VerificationError, RuntimeError) and issubclass(RefVE, RuntimeError)
+        finally:
+            sys.path.remove(ref)
+    for c in cases:
+        assert engine.failure_line(*c) == ref_line(*c)
+    rep = engine.DiffReport(0.5)
+    assert rep.clean and rep.first_bad_i is None
+    rep = engine.DiffReport(0.5, 3, 4, 1.0, 0.5)
+    assert not rep.clean
+    e = engine.VerificationError("C[ 1 ][ 2 ] != C_ref, 1E0, 2E0", m=3, n=4, k=5, algorithm="b200")
+    assert (e.diagnostic, e.m, e.n, e.k, e.algorithm) == ("C[ 1 ][ 2 ] != C_ref, 1E0, 2E0", 3, 4, 5, "b200")

@@ -55,6 +55,29 @@ def run_dev(torch, m, n, k, a, lda, b, ldb, c, ldc, **kw):
     torch.cuda.synchronize()
 
 
+def device_bound(torch, m, n, k, a, lda, b, ldb, c0, ldc, c=HEADLINE_C):
+    """The headline bound c * k * eps * (|A||B| + |C|)_max with the
+    magnitude computed on the device: the fast kernel on |A|,
+    |B| accumulating into |C|.  Every term is non-negative, so there is no
+    cancellation and the computed maximum is within a factor (1 + k eps) of
+    the exact one.  c0 is C before the update; buffers are ld * cols long."""
+    aa, bb, w = a.abs(), b.abs(), c0.abs()
+    run_dev(torch, m, n, k, aa, lda, bb, ldb, w, ldc)
+    mag = float(w.view(n, ldc)[:, :m].max())
+    del aa, bb, w
+    assert mag == mag and mag > 0.0
+    return c * k * EPS * mag
+
+
+def check_dev(torch, m, n, k, got, want, ld, bound):
+    """Device-side parity check (matrix.py:210-232 via my_dgemm_diff_report):
+    raises VerificationError with the reference's failure line at the first
+    offender, and fails on a NaN max."""
+    rep = engine.verify_device(m, n, k, got.data_ptr(), ld, want.data_ptr(), ld, bound)
+    assert rep.max_abs_diff <= bound, rep
+    return rep
+
+
 def headline_bound(m, n, k, a, lda, b, ldb, c0, ldc):
     A = oracle.valid_region(a, m, k, lda).T
     B = oracle.valid_region(b, k, n, ldb).T
@@ -87,8 +110,8 @@ def test_fill_matches_reference_goldens(torch_cuda, golden):
 
 # ------------------------------------------------------------ exact (bitwise)
 
-EXACT_KATS = ["cfg3d", "cfg1", "cfg2_256", "cfg2_768", "cfg2_1024", "cfg3b", "cfg3c", "cfg3a",
-              "cfg2_2048", "cfg4"]
+EXACT_KATS = ["cfg3d", "cfg1", "cfg2_256", "cfg2_768", "cfg2_1024", "cfg2_1280", "cfg2_1536", "cfg2_1792",
+              "cfg3b", "cfg3c", "cfg3a", "cfg2_2048", "cfg4"]
 
 
 @pytest.mark.parametrize("name", EXACT_KATS)
@@ -166,12 +189,11 @@ def test_fast_tiled_handles_skinny(torch_cuda, golden):
         m, n, k = kat["m"], kat["n"], kat["k"]
         lda, ldb, ldc = kat["lds"]
         a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc)
+        bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
         ce = c.clone()
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc, force_tiled=True)
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
-        bound = HEADLINE_C * k * EPS * 2.0 * k
-        mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
-        assert i is None and mx <= bound
+        check_dev(torch_cuda, m, n, k, c, ce, ldc, bound)
 
 
 def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
@@ -179,13 +201,11 @@ def test_fast_vs_exact_full_8192_and_samples(torch_cuda, golden):
     (bitwise-oracle) kernel, and the reference's sampled elements."""
     m = n = k = 8192
     a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    bound = device_bound(torch_cuda, m, n, k, a, m, b, k, c, m)
     ce = c.clone()
     run_dev(torch_cuda, m, n, k, a, m, b, k, c, m)
     run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
-    # |A||B|+|C| <= k + 1 for entries in [-1, 1)
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), m, ce.data_ptr(), m, bound)
-    assert i is None, (i, j, mx)
+    check_dev(torch_cuda, m, n, k, c, ce, m, bound)
     s = golden["sampled"]["cfg2_8192"]
     host_c = c.view(n, m)
     host_e = ce.view(n, m)
@@ -205,14 +225,15 @@ def test_cfg5_full_exact_samples_and_8_way_shards(torch_cuda, golden):
 
     torch = torch_cuda
     free, _ = torch.cuda.mem_get_info()
-    if free < 48 * 2**30:
-        pytest.skip("needs ~44 GB of device memory")
+    if free < 64 * 2**30:
+        pytest.skip("needs ~60 GB of device memory")
     s = golden["sampled"]["cfg5"]
     m, n, k = s["m"], s["n"], s["k"]
     a, b, c, _ = dev_operands(torch, m, n, k)
+    bound = device_bound(torch, m, n, k, a, m, b, k, c, m)
+    torch.cuda.empty_cache()
     fast = c.clone()
     run_dev(torch, m, n, k, a, m, b, k, fast, m)
-    bound = HEADLINE_C * k * EPS * (k + 1)  # |A||B|+|C| <= k + 1 for entries in [-1, 1)
     rows, cols = torch.tensor(s["rows"], device="cuda"), torch.tensor(s["cols"], device="cuda")
     pick = lambda x: x.view(n, m)[cols][:, rows].T.reshape(-1).cpu().tolist()  # row-major over (rows, cols)
     want = s["values"]
@@ -229,8 +250,7 @@ def test_cfg5_full_exact_samples_and_8_way_shards(torch_cuda, golden):
     del shard
     run_dev(torch, m, n, k, a, m, b, k, c, m, exact=True)  # c := the exact result
     assert pick(c) == want  # bitwise the reference's elements
-    mx, i, j = engine.max_abs_diff_device(m, n, fast.data_ptr(), m, c.data_ptr(), m, bound)
-    assert i is None, (i, j, mx)
+    check_dev(torch, m, n, k, fast, c, m, bound)
 
 
 def test_cfg4_full_fast_vs_exact(torch_cuda, golden):
@@ -239,13 +259,12 @@ def test_cfg4_full_fast_vs_exact(torch_cuda, golden):
     kat = golden["kat"]["cfg4"]
     m, n, k = kat["m"], kat["n"], kat["k"]
     a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+    bound = device_bound(torch_cuda, m, n, k, a, m, b, k, c, m)
     ce = c.clone()
     run_dev(torch_cuda, m, n, k, a, m, b, k, c, m)
     run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
     assert oracle.sha256_valid(ce.cpu().numpy(), m, n, m) == kat["sha256"]
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, c.data_ptr(), m, ce.data_ptr(), m, bound)
-    assert i is None, (i, j, mx)
+    check_dev(torch_cuda, m, n, k, c, ce, m, bound)
 
 
 @pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
@@ -276,9 +295,8 @@ def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     assert all(torch_cuda.equal(outs[0], o) for o in outs[1:])
     ce = c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, outs[0].data_ptr(), ldc, ce.data_ptr(), ldc, bound)
-    assert i is None, (i, j, mx)
+    bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch_cuda, m, n, k, outs[0], ce, ldc, bound)
     host = outs[3].cpu().numpy()
     if ldc > m:
         assert np.all(host.reshape(n, ldc)[:, m:] == -777.25)
@@ -686,18 +704,18 @@ def test_more_than_2_31_elements_of_c(torch_cuda):
     k = 16
     st = torch_cuda.cuda.current_stream().cuda_stream
     free, _ = torch_cuda.cuda.mem_get_info()
-    if free < 3 * m * n * 8 + (1 << 30):
-        pytest.skip("needs ~52 GB of free device memory")
+    if free < 4 * m * n * 8 + (1 << 30):
+        pytest.skip("needs ~70 GB of free device memory")
     a = dev_matrix(torch_cuda, m, k, m, 101)
     b = dev_matrix(torch_cuda, k, n, k, 102)
     c0 = dev_matrix(torch_cuda, m, n, m, 103)
     cf = c0.clone()
     run_dev(torch_cuda, m, n, k, a, m, b, k, cf, m)
+    bound = device_bound(torch_cuda, m, n, k, a, m, b, k, c0, m)
+    torch_cuda.cuda.empty_cache()
     ce = c0
     run_dev(torch_cuda, m, n, k, a, m, b, k, ce, m, exact=True)
-    bound = HEADLINE_C * k * EPS * (k + 1)  # |A|, |B|, |C| <= 1
-    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), m, ce.data_ptr(), m, bound)
-    assert i is None, (i, j, mx)
+    check_dev(torch_cuda, m, n, k, cf, ce, m, bound)
     # last element, bitwise against the naive order evaluated on the host
     row = a.view(k, m)[:, m - 1].cpu().numpy()
     col = b.view(n, k)[n - 1].cpu().numpy()
@@ -824,9 +842,8 @@ def test_few_columns_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     cf, ce = c.clone(), c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc)
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
-    assert i is None, (i, j, mx)
+    bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch_cuda, m, n, k, cf, ce, ldc, bound)
     again = c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc)
     assert torch_cuda.equal(again, cf)
@@ -856,9 +873,8 @@ def test_few_rows_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     cf, ce = c.clone(), c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cf, ldc, path=_capi.PATH_FEW_ROWS)
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
-    assert i is None, (i, j, mx)
+    bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch_cuda, m, n, k, cf, ce, ldc, bound)
     again = c.clone()
     run_dev(torch_cuda, m, n, k, a, lda, b, ldb, again, ldc, path=_capi.PATH_FEW_ROWS)
     assert torch_cuda.equal(again, cf)
@@ -896,9 +912,8 @@ def test_rows_dmma_kernel(torch_cuda, m, n, k, lda, ldb, ldc):
     cf, ce = c.clone(), c.clone()
     run_dev(torch, m, n, k, a, lda, b, ldb, cf, ldc, path=P)
     run_dev(torch, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
-    bound = HEADLINE_C * k * EPS * (k + 1)
-    mx, i, j = engine.max_abs_diff_device(m, n, cf.data_ptr(), ldc, ce.data_ptr(), ldc, bound)
-    assert i is None, (i, j, mx)
+    bound = device_bound(torch, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch, m, n, k, cf, ce, ldc, bound)
     again = c.clone()
     run_dev(torch, m, n, k, a, lda, b, ldb, again, ldc, path=P)
     assert torch.equal(again, cf)
@@ -944,15 +959,20 @@ def test_rows_dmma_keeps_negative_zero(torch_cuda):
 
 @pytest.mark.parametrize("m,n,k,alpha,beta", [(2048, 2048, 512, 1.5, -0.5), (2048, 2304, 700, 2.0, 0.0),
                                                (1280, 1280, 300, -1.0, 1.0)])
-def test_blas_epilogue_under_stream_k(torch_cuda, m, n, k, alpha, beta):
-    """The BLAS epilogue (product from zero, alpha/beta at the end) through
-    the stream-K schedule: cut tiles carry the partial product, the last
-    segment applies alpha and beta once; beta = 0 never reads a NaN C."""
+@pytest.mark.parametrize("epilogue", [False, True])
+def test_blas_epilogue_under_stream_k(torch_cuda, m, n, k, alpha, beta, epilogue):
+    """alpha / beta through the stream-K schedule (these shapes' tiles do not
+    fill the last wave).  Large tiled calls with beta != 0 default to the
+    reference-BLAS order (C := beta C, alpha folded into an operand, then the
+    accumulate contract), so `epilogue=True` (MY_DGEMM_BLAS_EPILOGUE) forces
+    the kernel epilogue for every case: cut tiles carry the partial product
+    from zero, the last segment applies alpha and beta once (reading C when
+    beta != 0); beta = 0 never reads a NaN C on either route."""
     torch = torch_cuda
     a, b, c, _ = dev_operands(torch, m, n, k)
     cin = c.clone() if beta != 0 else torch.full_like(c, float("nan"))
     out = cin.clone()
-    engine.dgemm("N", "N", m, n, k, alpha, a, m, b, k, beta, out, m)
+    engine.dgemm("N", "N", m, n, k, alpha, a, m, b, k, beta, out, m, epilogue=epilogue)
     torch.cuda.synchronize()
     A = a.view(k, m).T
     B = b.view(n, k).T
@@ -998,9 +1018,8 @@ def test_fuzz_random_shapes_fast_vs_exact(torch_cuda, seed):
         fast, exact = c.clone(), c.clone()
         run_dev(torch, m, n, k, a, lda, b, ldb, fast, ldc)
         run_dev(torch, m, n, k, a, lda, b, ldb, exact, ldc, exact=True)
-        bound = HEADLINE_C * k * EPS * (k + 1)  # |A||B|+|C| <= k + 1 for entries in [-1, 1)
-        mx, i, j = engine.max_abs_diff_device(m, n, fast.data_ptr(), ldc, exact.data_ptr(), ldc, bound)
-        assert i is None, ((m, n, k, lda, ldb, ldc), i, j, mx)
+        bound = device_bound(torch, m, n, k, a, lda, b, ldb, c, ldc)
+        check_dev(torch, m, n, k, fast, exact, ldc, bound)
         if ldc > m:
             assert bool((fast.view(n, ldc)[:, m:] == -777.25).all()), (m, n, k)
         tiled = []
@@ -1031,3 +1050,128 @@ def test_signed_zero_is_plan_invariant_and_matches_the_oracle(torch_cuda, m, n, 
         cc = c.clone()
         run_dev(torch, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True)
         assert bool(torch.signbit(cc.view(n, ldc)[:, :m]).all()), strips
+
+
+# ------------------------------------------- the device checker's own controls
+
+
+def _host_report(got, want, m, n, ld, tol):
+    return oracle.max_abs_diff(got.cpu().numpy(), want.cpu().numpy(), m, n, ld, tol=tol)
+
+
+def _same_report(dev, host):
+    same_max = (dev.max_abs_diff == host.max_abs_diff
+                or (dev.max_abs_diff != dev.max_abs_diff and host.max_abs_diff != host.max_abs_diff))
+    assert same_max, (dev, host)
+    assert (dev.first_bad_i, dev.first_bad_j) == (host.first_bad_i, host.first_bad_j), (dev, host)
+    if not host.clean:
+        assert np.array_equal(np.float64(dev.value_got), np.float64(host.value_got), equal_nan=True)
+        assert dev.value_expected == host.value_expected
+        assert (engine.failure_line(dev.first_bad_i, dev.first_bad_j, dev.value_got, dev.value_expected)
+                == oracle.failure_line(host.first_bad_i, host.first_bad_j, host.value_got, host.value_expected))
+
+
+TOL = 2.0**-30
+
+
+def _plants(m, n):
+    """Planted (i, j, kind) mismatch sets; kinds: 'at' = difference exactly
+    the tolerance (not an offender under the strict > rule), 'above' = one ulp
+    of 0.5 past it, 'big', 'nan', 'inf'.  Positions: first and last element,
+    a 128-row tile boundary, an 8-way jc shard boundary, the last column."""
+    sh = (n // 8) if n >= 8 else n - 1
+    return {
+        "first": [(0, 0, "big")],
+        "last": [(m - 1, n - 1, "big")],
+        "tile_edge": [(127, 1, "at"), (128, 1, "above"), (m - 1, n - 1, "big")],
+        "shard_edge": [(0, sh - 1, "at"), (5, sh, "above")],
+        "just_above_after_at": [(3, 0, "at"), (4, 0, "at"), (m - 2, n - 1, "above")],
+        "only_at": [(1, 1, "at"), (m - 1, n - 1, "at")],
+        "nan_only": [(7, 2, "nan")],
+        "nan_then_above": [(2, 0, "nan"), (9, n - 1, "above")],
+        "inf": [(m // 2, n // 2, "inf")],
+        "clean": [],
+    }
+
+
+@pytest.mark.parametrize("m,n,ld", [(1000, 777, 1003), (4096, 8192, 4096)])
+@pytest.mark.parametrize("case", list(_plants(1000, 777)))
+def test_device_checker_negative_control(torch_cuda, m, n, ld, case):
+    """my_dgemm_diff_report (the checker every full-matrix GPU parity test
+    relies on) against oracle.max_abs_diff (matrix.py:210-232) on planted
+    mismatches: same max (NaN included), same first offender in column-major
+    order under the strict > tol rule, same offender values and the same
+    reference failure line (bench.py:84-86); verify_device raises with that
+    line, or on a NaN max.  A checker stubbed to 'clean' fails every
+    case but 'clean' and 'only_at'."""
+    torch = torch_cuda
+    want = dev_matrix(torch, m, n, ld, 5, canary=-777.25)
+    got = want.clone()
+    for i, j, kind in _plants(m, n)[case]:
+        t = j * ld + i
+        want[t] = 0.5
+        got[t] = {"at": 0.5 + TOL, "above": 0.5 + TOL + 2.0**-53, "big": 3.0,
+                  "nan": float("nan"), "inf": float("inf")}[kind]
+    dev = engine.diff_report_device(m, n, got.data_ptr(), ld, want.data_ptr(), ld, TOL)
+    host = _host_report(got, want, m, n, ld, TOL)
+    _same_report(dev, host)
+    expect_bad = [(i, j) for i, j, kind in _plants(m, n)[case] if kind in ("above", "big", "inf")]
+    if expect_bad:
+        first = min(expect_bad, key=lambda p: p[1] * m + p[0])
+        assert (dev.first_bad_i, dev.first_bad_j) == first
+        with pytest.raises(engine.VerificationError) as ei:
+            engine.verify_device(m, n, 7, got.data_ptr(), ld, want.data_ptr(), ld, TOL)
+        assert ei.value.diagnostic == oracle.failure_line(host.first_bad_i, host.first_bad_j, host.value_got,
+                                                          host.value_expected)
+        assert ei.value.diagnostic.startswith(f"C[ {first[0]} ][ {first[1]} ] != C_ref, ")
+    else:
+        assert dev.clean
+        if case.startswith("nan"):
+            assert dev.max_abs_diff != dev.max_abs_diff
+            with pytest.raises(engine.VerificationError, match="NaN"):
+                engine.verify_device(m, n, 7, got.data_ptr(), ld, want.data_ptr(), ld, TOL)
+        else:
+            engine.verify_device(m, n, 7, got.data_ptr(), ld, want.data_ptr(), ld, TOL)
+    # the canaries in the padding rows never enter the comparison
+    if ld > m:
+        got.view(n, ld)[:, m:] = 1e300
+        again = engine.diff_report_device(m, n, got.data_ptr(), ld, want.data_ptr(), ld, TOL)
+        assert (again.first_bad_i, again.first_bad_j) == (dev.first_bad_i, dev.first_bad_j)
+
+
+def test_device_checker_tolerance_zero_finds_first_difference(torch_cuda):
+    """tol = 0 (the reference default): the first differing element."""
+    torch = torch_cuda
+    m, n = 300, 200
+    want = dev_matrix(torch, m, n, m, 6)
+    got = want.clone()
+    got[77 * m + 150] = float(got[77 * m + 150]) * (1 + 2.0**-50)
+    got[150 * m + 3] += 1.0
+    dev = engine.diff_report_device(m, n, got.data_ptr(), m, want.data_ptr(), m, 0.0)
+    assert (dev.first_bad_i, dev.first_bad_j) == (150, 77)
+    _same_report(dev, _host_report(got, want, m, n, m, 0.0))
+
+
+# ------------------------------ every timed point of the cfg2 sweep, full matrix
+
+CFG2_SIZES = list(range(256, 8192 + 1, 256))
+
+
+@pytest.mark.parametrize("s", CFG2_SIZES)
+def test_cfg2_sweep_point_exact_kat_and_fast_full(torch_cuda, golden, s):
+    """Every size the sweep times (BASELINE configs[1]; the reference's
+    run_sweep verifies every timed shape, bench.py:140-156): the exact kernel
+    reproduces the reference's C bit for bit (SHA-256 of C from
+    gemm_goto_parallel, tests/golden/make_golden.py), and every element of
+    the fast result lies within the headline bound (c = 2, magnitude on the
+    device) of it."""
+    torch = torch_cuda
+    kat = golden["kat"]["cfg1" if s == 512 else f"cfg2_{s}"]
+    assert (kat["m"], kat["n"], kat["k"]) == (s, s, s)
+    a, b, c, _ = dev_operands(torch, s, s, s)
+    bound = device_bound(torch, s, s, s, a, s, b, s, c, s)
+    fast, exact = c.clone(), c
+    run_dev(torch, s, s, s, a, s, b, s, fast, s)
+    run_dev(torch, s, s, s, a, s, b, s, exact, s, exact=True)
+    assert oracle.sha256_valid(exact.cpu().numpy(), s, s, s) == kat["sha256"]
+    check_dev(torch, s, s, s, fast, exact, s, bound)

@@ -145,3 +145,62 @@ def test_syrk_vs_numpy(uplo, trans, n, k, alpha, beta):
     other = got[~mask]
     assert np.all(np.isnan(other)) if beta == 0.0 else np.array_equal(other, C[~mask])
     assert np.all(dC.cpu().numpy().reshape(n, ldc)[:, n:] == -777.25)
+
+
+def _tri_only_product(opA, B, side, lower):
+    """op(A) B (left) or B op(A) (right) summing only the triangle's products:
+    products outside the triangle are dropped, not multiplied by zero, as
+    reference BLAS never reads the other triangle (0 * Inf would be NaN)."""
+    na = opA.shape[0]
+    mask = np.tril(np.ones((na, na), bool)) if lower else np.triu(np.ones((na, na), bool))
+    with np.errstate(invalid="ignore", over="ignore"):
+        if side == "L":  # W[r, j] = sum_c opA[r, c] B[c, j]
+            prod = opA[:, :, None] * B[None, :, :]
+            return np.where(mask[:, :, None], prod, 0.0).sum(axis=1)
+        prod = B[:, :, None] * opA[None, :, :]  # W[r, cc] = sum_c B[r, c] opA[c, cc]
+        return np.where(mask[None, :, :], prod, 0.0).sum(axis=1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("side,uplo,trans", list(itertools.product("LR", "LU", "NT")))
+def test_trmm_nonfinite_b_reads_triangle_only(side, uplo, trans):
+    """Inf / -Inf / NaN in B: the dense 512 diagonal-block
+    multiply must not turn 0 * Inf from the unreferenced triangle into NaN.
+    Result against a triangle-only evaluation: finite entries within the
+    bound, the non-finite pattern (which vectors are Inf / NaN, and the sign
+    of each Inf) identical."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    m, n = (600, 24) if side == "L" else (24, 600)  # the triangle's order > 256: the dense-block path
+    rng = np.random.default_rng(17)
+    na = m if side == "L" else n
+    lda, ldb = na + 1, m + 2
+    tri, abuf = _tri_matrix(rng, na, lda, uplo, "N")
+    B = rng.uniform(-1, 1, (m, n))
+    if side == "L":  # one non-finite per column vector, in different 512-blocks' reach
+        B[5, 3], B[300, 7], B[550, 11] = np.inf, -np.inf, np.nan
+        B[599, 20] = np.inf
+    else:
+        B[3, 5], B[7, 300], B[11, 550] = np.inf, -np.inf, np.nan
+        B[20, 599] = np.inf
+    bbuf = np.full((n, ldb), -777.25)
+    bbuf[:, :m] = B.T
+    dA = torch.from_numpy(abuf.ravel()).cuda()
+    dB = torch.from_numpy(bbuf.ravel().copy()).cuda()
+    alpha = -1.5
+    engine.dtrmm(side, uplo, trans, "N", m, n, alpha, dA, lda, dB, ldb)
+    torch.cuda.synchronize()
+    got = dB.cpu().numpy().reshape(n, ldb)[:, :m].T
+    opA = _op(tri, trans)
+    lower = (uplo == "L") != (trans == "T")
+    want = _tri_only_product(opA, alpha * B, side, lower)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    assert np.array_equal(np.isposinf(got), np.isposinf(want))
+    assert np.array_equal(np.isneginf(got), np.isneginf(want))
+    fin = np.isfinite(want)
+    assert fin.sum() > 0.5 * fin.size and (~fin).sum() > 0
+    Bf = np.where(np.isfinite(B), B, 0.0)
+    bound = 4 * na * EPS * 1.5 * (np.abs(opA) @ np.abs(Bf) if side == "L" else np.abs(Bf) @ np.abs(opA)).max()
+    assert np.abs(got[fin] - want[fin]).max() <= bound
+    assert np.all(dB.cpu().numpy().reshape(n, ldb)[:, m:] == -777.25)

@@ -70,7 +70,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q):
+def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q, host=False):
     import oracle
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -92,7 +92,16 @@ def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q):
             oracle.naive(m_, nloc, kc, A_.numpy(), lda_, B_.numpy(), ldb_, C_.numpy(), ldc_)
 
         drv = ShardedDgemm(plan, rank, compute=compute, overlap=overlap)
-        drv.step(A, lda, B_local, ldb, C_local, ldc)
+        if host:  # step_host: operands start in host buffers, device-side buffers hold junk
+            hA, hB, hC = A.clone(), B_local.clone(), C_local.clone()
+            A.fill_(-1.0)
+            B_local.fill_(-2.0)
+            C_local.fill_(-3.0)
+            out = drv.step_host(hA, A, lda, hB, B_local, ldb, hC, C_local, ldc)
+            assert out is hC
+            C_local = hC
+        else:
+            drv.step(A, lda, B_local, ldb, C_local, ldc)
         # valid region of A arrived; padding rows were never sent
         got_a = oracle.valid_region(A.numpy(), m, k, lda)
         out_q.put((rank, j0, j1, C_local.numpy().copy(), calls,
@@ -101,20 +110,23 @@ def _worker(rank, world, port, shape, lds, k_chunk, overlap, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,lds,k_chunk,overlap", [
-    ((37, 300, 71), (44, 76, 40), 32, True),
-    ((16, 129, 50), (16, 50, 16), 16, True),   # few-row path: one k chunk (only the tiled family chunks k)
-    ((20, 129, 50), (20, 50, 21), 16, True),
-    ((37, 300, 71), (44, 76, 40), 32, False),
+@pytest.mark.parametrize("shape,lds,k_chunk,overlap,host", [
+    ((37, 300, 71), (44, 76, 40), 32, True, False),
+    ((16, 129, 50), (16, 50, 16), 16, True, False),   # few-row path: one k chunk (only the tiled family chunks k)
+    ((20, 129, 50), (20, 50, 21), 16, True, False),
+    ((37, 300, 71), (44, 76, 40), 32, False, False),
+    ((37, 300, 71), (44, 76, 40), 32, True, True),    # step_host: uploads, chunked broadcast, download
+    ((37, 300, 71), (44, 76, 40), 32, False, True),
 ])
-def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk, overlap):
+def test_gloo_world2_sharded_step_bitwise_equals_oracle(shape, lds, k_chunk, overlap, host):
     import oracle
 
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, lds, k_chunk, overlap, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, lds, k_chunk, overlap, q, host))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
