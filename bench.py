@@ -1,26 +1,31 @@
 """bench.py -- the driver contract for the my_dgemm path on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload cfg2_8192|cfg5|cfg4|cfg3a] [--no-cpu-baseline]
+                  [--workload cfg5|cfg2_8192|cfg4|cfg3a] [--scaling strong|weak]
+                  [--exchange all|nccl|chain] [--no-cpu-baseline] [--no-e2e]
 
-For N>1 launch under torchrun (one rank per GPU, NCCL).  One JSON line on
-rank 0.
+N > 1 outside torchrun: bench.py starts the N ranks itself (torch.distributed
+.run on 127.0.0.1, one process per GPU, NCCL); under torchrun WORLD_SIZE must
+equal --gpus.  One JSON line on rank 0.
 
-Workload (BASELINE.json configs[1], the size sweep's headline point): DGEMM
-C := A*B + C, m = k = 8192, fp64, column-major, tight leading dimensions,
-operands from the reference generator (seed 42, splitmix64-v1, generated on
-the device bit-exactly).  At N ranks the problem grows by columns (weak
-scaling): n = 8192*N, rank g owns columns [8192g, 8192(g+1)) of B and C, A
-lives on rank 0 and is broadcast over NCCL inside every step before the
-per-rank GEMM (--overlap: in k-chunks under the GEMM; paper_1609_00076_b200/
-multi.py explains why that is not the default).  A step
-is one full C += A*B.  Inputs (3 x 512 MiB per rank) exceed the 126 MB L2,
-so no flush is needed between steps.
+Workload (default): SURVEY 8e's scaling problem, BASELINE configs[4] -- DGEMM
+C := A*B + C, m = n = k = 32768, fp64, column-major, tight leading
+dimensions, operands from the reference generator (seed 42, splitmix64-v1,
+generated on the device bit-exactly; 8.6 GB per matrix).  Strong scaling:
+rank g owns the column panel split_columns(32768, N)[g] of B and C; A lives
+on rank 0 and reaches the others inside every timed step.  At N > 1 every
+exchange schedule is timed in the same run -- the serialized NCCL broadcast,
+the chunked NCCL broadcast under the GEMM (with and without SMs reserved
+for NCCL) and the copy-engine chain over NVLink peer memory -- and the
+fastest is the value (the others under alt_exchange).  A step is one full
+C += A*B.  Inputs exceed the 126 MB L2, so no flush is needed.
 
 value  = 2*m*n*k * K / max-over-ranks device time (CUDA events), GFLOP/s.
-e2e    = the same metric through the public host API (my_dgemm_ex with host
-         pointers from pinned memory: H2D of A, B, C and D2H of C inside every
-         step), wall-clock, rank 0 / per-rank host call at N>1.
+e2e    = the same metric through the public host API, host buffers pinned,
+         wall clock, max over ranks: N = 1 my_dgemm_ex with host pointers
+         (H2D of A, B, C and D2H of C inside every call); N > 1
+         ShardedDgemm.step_host (B / C panels per rank, A from the root's
+         host memory into the exchange, C panels back).
 roofline: dominant kernel = dgemm_fast_kernel; bound "tensor" (the FP64 DMMA
          pipe); achieved = 2mnk per launch / mean launch time (CUDA events on
          the launch stream); peak = 37.22 TFLOP/s nominal FP64
@@ -28,9 +33,9 @@ roofline: dominant kernel = dgemm_fast_kernel; bound "tensor" (the FP64 DMMA
          measured 37.10, profiles/fp64_peak_r01.txt).  MEASURED_PEAKS.json
          holds no FP64 figure.
 cpu_baseline: the reference's own CPU path (oracle/_ref: gemmforge
-         gemm_goto_parallel, compiled backend, all host threads) on a column
-         slab of the same workload; "port" (oracle/ C restatement) if the
-         reference package is absent.
+         gemm_goto_parallel, compiled backend, all host threads) on a k-slab
+         of the same workload (see CpuReference); "port" (oracle/ C
+         restatement) if the reference package is absent.
 `--impl reference` times that CPU path as the reference arm.
 """
 
@@ -43,6 +48,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
@@ -130,15 +137,27 @@ class ClockSampler:
 
 
 class CpuReference:
-    """The reference's CPU path on column slabs of the workload.
+    """The reference's CPU path on a k-slab of the workload.
 
     kind "reference": gemmforge.parallel.gemm_goto_parallel from oracle/_ref
     (the unmodified reference, compiled backend, GotoParams() defaults, all
-    host threads, loop ic when ceil(m/64) >= T else jr -- BASELINE.md 4),
-    timed per the reference protocol (bench.py:109-123: C reset outside the
-    timed region).  kind "port": oracle/liboracle.so's C restatement of the
-    same five-loop algorithm.  A (m x k) is generated once and reused.
+    host threads, loop ic when ceil(m/64) >= T else jr -- BASELINE.md 4).
+    kind "port": oracle/liboracle.so's C restatement of the same algorithm.
+
+    A sample is d (a multiple of kc = 256) consecutive pc iterations of the
+    reference's own loop nest over the WHOLE m x n problem: C += A[:, :d] *
+    B[:d, :] with every jc panel (nc = 4096 columns), every ic block, the same
+    packing, barriers and C traffic per pc iteration as the full call, which
+    is k/kc such iterations (goto.py:212-229, parallel.py:183-199).  So the
+    sample's rate is the full problem's rate, which a column slab narrower
+    than nc would understate (each packed A block would feed fewer columns).
+    Operands come from the reference generator at their positions in the full
+    matrices: A's first d columns, B's first d rows (ld = k, so the strides
+    are the full problem's), C whole.  C is not reset between runs (the
+    values do not change the work).
     """
+
+    KC = 256  # GotoParams().kc
 
     def __init__(self, m: int, n: int, k: int):
         self.m, self.n, self.k = m, n, k
@@ -151,73 +170,85 @@ class CpuReference:
             from gemmforge.backends import available_backends
             use_ref = "c" in available_backends()
         self.use_ref = use_ref
-        self._a = None
-        self._slabs = {}
+        self._c = None
+        self._ab = (0, None, None)
 
-    def _operands(self, ns):
+    def _operands(self, d):
         m, n, k = self.m, self.n, self.k
         if self.use_ref:
             from gemmforge.bench import _operand_seed
-            from gemmforge.matrix import alloc_matrix, fill_random
+            from gemmforge.matrix import Matrix, alloc_matrix, fill_random, random_values
 
-            if self._a is None:
-                self._a = fill_random(alloc_matrix(m, k), _operand_seed(SEED, 1, m, n, k))
-            if ns not in self._slabs:
-                self._slabs = {ns: (fill_random(alloc_matrix(k, ns), _operand_seed(SEED, 2, m, n, k)),
-                                    fill_random(alloc_matrix(m, ns), _operand_seed(SEED, 3, m, n, k)))}
-        else:
-            import oracle
+            if self._c is None:
+                self._c = fill_random(alloc_matrix(m, n), _operand_seed(SEED, 3, m, n, k))
+            if self._ab[0] < d:
+                a = fill_random(alloc_matrix(m, d), _operand_seed(SEED, 1, m, n, k))  # A[:, :d]
+                b = alloc_matrix(d, n, k)  # B[:d, :] with the full problem's ld
+                sb = _operand_seed(SEED, 2, m, n, k)
+                for j in range(n):
+                    b.data[j * k:j * k + d] = random_values(sb, d, start=j * k)
+                self._ab = (d, a, b)
+            _, a, b = self._ab
+            return Matrix(m, d, m, a.data[:m * d]), Matrix(d, n, k, b.data), self._c
+        import oracle
 
-            if self._a is None:
-                self._a = oracle.fill(oracle.alloc(m, k), m, k, m, oracle.operand_seed(SEED, 1, m, n, k))
-            if ns not in self._slabs:
-                self._slabs = {ns: (
-                    oracle.fill(oracle.alloc(k, ns), k, ns, k, oracle.operand_seed(SEED, 2, m, n, k)),
-                    oracle.fill(oracle.alloc(m, ns), m, ns, m, oracle.operand_seed(SEED, 3, m, n, k)))}
-        return (self._a, *self._slabs[ns])
+        if self._c is None:
+            self._c = oracle.fill(oracle.alloc(m, n), m, n, m, oracle.operand_seed(SEED, 3, m, n, k))
+        if self._ab[0] < d:
+            a = oracle.fill(oracle.alloc(m, d), m, d, m, oracle.operand_seed(SEED, 1, m, n, k))
+            b = np.zeros(k * (n - 1) + d)
+            sb = oracle.operand_seed(SEED, 2, m, n, k)
+            for j in range(n):
+                b[j * k:j * k + d] = oracle.random_values(sb, d, start=j * k)
+            self._ab = (d, a, b)
+        return self._ab[1], self._ab[2], self._c
 
-    def time_slab(self, ns: int) -> float:
-        a, b, c0 = self._operands(ns)
-        m, k, T = self.m, self.k, self.threads
+    def time_sample(self, d: int) -> float:
+        a, b, c = self._operands(d)
+        m, n, k, T = self.m, self.n, self.k, self.threads
         if self.use_ref:
             from gemmforge.goto import GotoParams
-            from gemmforge.matrix import copy_matrix
             from gemmforge.parallel import gemm_goto_parallel, make_plan
 
             p = GotoParams()
-            plan = (make_plan("ic", T, m, p.mc) if -(-m // p.mc) >= T else make_plan("jr", T, ns, p.nr))
-            c = copy_matrix(c0)  # reset outside the timed region
+            plan = (make_plan("ic", T, m, p.mc) if -(-m // p.mc) >= T else make_plan("jr", T, n, p.nr))
             t0 = time.perf_counter()
             gemm_goto_parallel(a, b, c, p, plan)
             return time.perf_counter() - t0
         import oracle
 
-        c = c0.copy()
         t0 = time.perf_counter()
-        oracle.goto(m, ns, k, a, m, b, k, c, m, threads=T)
+        oracle.goto(m, n, d, a, m, b, k, c, m, threads=T)
         return time.perf_counter() - t0
 
-    def slab_for(self, seconds: float) -> int:
-        """Columns for ~`seconds` of work, calibrated on a 16-column slab."""
-        ns0 = max(1, min(self.n, 16))
-        t0 = self.time_slab(ns0)
-        rate = 2.0 * self.m * ns0 * self.k / t0
-        return int(max(ns0, min(self.n, seconds * rate / (2.0 * self.m * self.k))))
+    def flop(self, d: int) -> float:
+        return 2.0 * self.m * self.n * d
 
-    def info(self, ns: int, t: float, reps: int) -> dict:
-        m, k = self.m, self.k
+    def depth_for(self, seconds: float) -> int:
+        """k-slab depth (a multiple of kc, at most k) for ~`seconds` of work,
+        calibrated on one pc iteration."""
+        d0 = min(self.k, self.KC)
+        t0 = self.time_sample(d0)
+        want = seconds * self.flop(d0) / t0 / (2.0 * self.m * self.n)
+        d = int(want // self.KC) * self.KC
+        return max(d0, min(self.k, d))
+
+    def info(self, d: int, t: float, reps: int) -> dict:
+        m, n, k = self.m, self.n, self.k
+        iters = -(-k // self.KC)
         return {"kind": "reference" if self.use_ref else "port", "cores": self.threads,
-                "sample": f"column slab B[:, :{ns}] of m={m} k={k} (n={self.n}); "
-                          f"{2.0 * m * ns * k:.3e} flop per run; best {t:.2f} s of {reps}; "
+                "sample": f"k-slab C += A[:, :{d}] B[:{d}, :] over the whole {m}x{n} C (k={k}): "
+                          f"{-(-d // self.KC)} of the full call's {iters} pc iterations, every jc panel and ic "
+                          f"block; {self.flop(d):.3e} flop per run; best {t:.2f} s of {reps}; "
                           + ("gemmforge gemm_goto_parallel (oracle/_ref, compiled backend), GotoParams() defaults"
                              if self.use_ref else "oracle/liboracle.so oracle_goto (C port of goto/parallel)")}
 
 
 def cpu_reference_rate(m: int, n: int, k: int, target_s: float = 12.0, reps: int = 1):
     ref = CpuReference(m, n, k)
-    ns = ref.slab_for(target_s / max(1, reps))
-    t = min(ref.time_slab(ns) for _ in range(max(1, reps)))
-    return 2.0 * m * ns * k / t / 1e9, ref.info(ns, t, reps)
+    d = ref.depth_for(target_s / max(1, reps))
+    t = min(ref.time_sample(d) for _ in range(max(1, reps)))
+    return ref.flop(d) / t / 1e9, ref.info(d, t, reps)
 
 
 def run_reference_arm(args):
@@ -225,28 +256,33 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     m, n_rank, k = WORKLOADS[args.workload]
-    n = n_rank if args.strong else n_rank * max(world, args.gpus)  # the GPU arm's whole-job problem
+    n = n_rank if args.scaling == "strong" else n_rank * max(world, args.gpus)  # the GPU arm's whole-job problem
     # each step a bounded slab so W+K steps finish within a few minutes
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     ref = CpuReference(m, n, k)
-    ns = ref.slab_for(per_step)
+    d = ref.depth_for(per_step)
     rates, times = [], []
     for s in range(args.warmup + args.steps):
-        t = ref.time_slab(ns)
+        t = ref.time_sample(d)
         if s >= args.warmup:
-            rates.append(2.0 * m * ns * k / t / 1e9)
+            rates.append(ref.flop(d) / t / 1e9)
             times.append(t)
-    info = ref.info(ns, min(times), len(times))
+    info = ref.info(d, min(times), len(times))
     value = sum(rates) / len(rates)
     flop_step = 2.0 * m * n * k
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(flop_step / (value * 1e9) * 1e3, 3),
-        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
+        # a step is one timed k-slab of the whole problem (d of its k/256 pc
+        # iterations); the whole problem's time is extrapolated from its rate
+        "ms_per_step": round(sum(times) / len(times) * 1e3, 3),
+        "ms_per_step_full_problem_extrapolated": round(flop_step / (value * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator, seed 42)",
         "config": {"workload": args.workload, "m": m, "n": n, "k": k, "lda": m, "ldb": k, "ldc": m,
-                   "layout": "column-major", "note": "each step times a column slab (cpu_baseline.sample)"},
+                   "layout": "column-major", "sample_k_depth": d,
+                   "note": "each step times the k-slab C += A[:, :sample_k_depth] B[:sample_k_depth, :] of this "
+                           "problem (cpu_baseline.sample)"},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, **info},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -257,6 +293,30 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------- GPU arm
 
 
+def _schedules(args, world):
+    """Exchange schedules the run times.  N = 1: no exchange.  N > 1: the
+    serialized NCCL broadcast, the chunked NCCL broadcast under the GEMM
+    (with and without SMs reserved for NCCL), and the copy-engine chain
+    over NVLink peer memory -- or only the one --exchange names."""
+    if world == 1:
+        return [("single", dict(exchange="nccl", overlap=False, reserve_sms=0))]
+    every = [
+        ("nccl", dict(exchange="nccl", overlap=False, reserve_sms=0)),
+        ("nccl-overlap", dict(exchange="nccl", overlap=True, reserve_sms=0)),
+        (f"nccl-overlap-reserve{args.reserve_sms or 8}",
+         dict(exchange="nccl", overlap=True, reserve_sms=args.reserve_sms or 8)),
+        ("chain", dict(exchange="chain", overlap=True, reserve_sms=0)),
+    ]
+    if args.exchange == "all":
+        return every
+    if args.exchange == "chain":
+        return [("chain", dict(exchange="chain", overlap=True, reserve_sms=0))]
+    name = "nccl-overlap" if args.overlap else "nccl"
+    if args.overlap and args.reserve_sms:
+        name += f"-reserve{args.reserve_sms}"
+    return [(name, dict(exchange="nccl", overlap=args.overlap, reserve_sms=args.reserve_sms))]
+
+
 def run_b200_arm(args):
     import torch
     import torch.distributed as dist
@@ -265,17 +325,29 @@ def run_b200_arm(args):
     from paper_1609_00076_b200.multi import ShardedDgemm, make_shard_plan
 
     rank, world, local = env_rank()
-    if world != args.gpus:
-        args.gpus = world
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # --emulate-world W (tests, one GPU): a one-rank NCCL group runs rank 0's
+    # share of a W-way split through every N > 1 code path (schedules,
+    # chunked broadcasts on NCCL's stream, step_host, the line's N > 1 keys);
+    # no data moves and the numbers describe rank 0's panel only.
+    pw = args.emulate_world or world  # the world the plan is cut for
+    use_pg = world > 1 or args.emulate_world > 0
+    if use_pg:
+        # rank 0 logs NCCL's communicator setup ("nRanks N"); the others stay quiet
+        os.environ.setdefault("NCCL_DEBUG", "INFO" if rank == 0 else "WARN")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29577")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     lib = _capi.load()
 
     m, n_rank, k = WORKLOADS[args.workload]
-    n_total = n_rank if args.strong else n_rank * world  # strong: the workload's n split over the ranks
-    plan = make_shard_plan(m, n_total, k, world, root=0, k_chunk=args.k_chunk)
+    strong = args.scaling == "strong"
+    n_total = n_rank if strong else n_rank * pw
+    plan = make_shard_plan(m, n_total, k, pw, root=0, k_chunk=args.k_chunk)
     j0, j1 = plan.local(rank)
     nloc = j1 - j0
     stream = torch.cuda.current_stream(dev)
@@ -285,185 +357,319 @@ def run_b200_arm(args):
     B = torch.empty(k * nloc, dtype=torch.float64, device=dev)
     C = torch.empty(m * nloc, dtype=torch.float64, device=dev)
     seeds = [engine.operand_seed(SEED, r, m, n_total, k) for r in (1, 2, 3)]
-    if rank == 0:
-        engine.fill_random_device(A.data_ptr(), m, k, m, seeds[0], 0, st)
-    else:
-        A.fill_(float("nan"))  # must be overwritten by the broadcast
+
+    def fill_a():
+        if rank == 0:
+            engine.fill_random_device(A.data_ptr(), m, k, m, seeds[0], 0, st)
+        else:
+            A.fill_(float("nan"))  # must be overwritten by the exchange
+
+    fill_a()
     engine.fill_random_device(B.data_ptr(), k, nloc, k, seeds[1], j0, st)
     engine.fill_random_device(C.data_ptr(), m, nloc, m, seeds[2], j0, st)
     torch.cuda.synchronize()
 
-    # per-launch timing of the dominant kernel: events around each GEMM launch
-    launch_events: list[tuple] = []
-
-    def timed_compute(mm, nl, kc, A_, lda, B_, ldb, C_, ldc):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        engine.dgemm_device(mm, nl, kc, A_.data_ptr(), lda, B_.data_ptr(), ldb, C_.data_ptr(), ldc,
-                            st, path=drv.path)
-        e1.record(stream)
-        launch_events.append((e0, e1, kc))
-
-    drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=args.overlap, reserve_sms=args.reserve_sms)
-    close_chain = None
-    if world > 1 and args.exchange == "chain":  # A over NVLink by the copy engines (peer.py)
-        from paper_1609_00076_b200.peer import connect_chain
-
-        chain, close_chain = connect_chain(A, drv.chain_spans(m), rank, world, root=0)
-        drv.attach_chain(chain)
-
-    def step():
-        drv.step(A, m, B, k, C, m)
-
     def barrier():
-        if world > 1:
+        if use_pg:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    launch_events.clear()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = lib.my_dgemm_kernel_launches()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    barrier()
-    t_start.record(stream)
-    for _ in range(args.steps):
-        step()
-    t_end.record(stream)
-    barrier()
-    launches = lib.my_dgemm_kernel_launches() - launches0
-    clk = clocks.stop()
-    ms = t_start.elapsed_time(t_end)
-    kern_ms = [e0.elapsed_time(e1) for e0, e1, _ in launch_events]
-    kern_flop = [2.0 * m * nloc * kc for _, _, kc in launch_events]
-    if world > 1:
-        t = torch.tensor([ms, float(launches)], dtype=torch.float64, device=dev)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms_max, launches_total = float(mx[0]), int(sm[1])
-    else:
-        ms_max, launches_total = ms, int(launches)
-    flop_step = 2.0 * m * n_total * k
-    value = flop_step * args.steps / (ms_max * 1e-3) / 1e9
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if use_pg:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t]
 
-    exchange_name = ("copy-engine chain over NVLink peer memory" if args.exchange == "chain"
-                     else "NCCL broadcast")
-    if close_chain is not None:
-        close_chain()
+    def sum_over_ranks(v):
+        t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+        if use_pg:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t[0])
+
+    launch_events: list[tuple] = []
+
+    def make_driver(opts):
+        def timed_compute(mm, nl, kc, A_, lda, B_, ldb, C_, ldc):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            cur = torch.cuda.current_stream(dev)
+            e0.record(cur)
+            engine.dgemm_device(mm, nl, kc, A_.data_ptr(), lda, B_.data_ptr(), ldb, C_.data_ptr(), ldc,
+                                cur.cuda_stream, path=drv.path)
+            e1.record(cur)
+            launch_events.append((e0, e1, kc))
+
+        drv = ShardedDgemm(plan, rank, compute=timed_compute, overlap=opts["overlap"],
+                           reserve_sms=opts["reserve_sms"])
+        close = None
+        if world > 1 and opts["exchange"] == "chain":  # A over NVLink by the copy engines (peer.py)
+            from paper_1609_00076_b200.peer import connect_chain
+
+            chain, close = connect_chain(A, drv.chain_spans(m), rank, world, root=0)
+            drv.attach_chain(chain)
+        return drv, close
+
+    def time_steps(step_fn, steps):
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(steps):
+            step_fn()
+        t1.record(stream)
+        barrier()
+        return t0.elapsed_time(t1)
+
+    results = {}  # name -> dict(ms, kern_ms, kern_flop, launches)
+    clock_lines = {}
+    flop_step = 2.0 * m * (n_total if pw == world else nloc) * k  # emulated: rank 0's share only
+    done = threading.Event()
+    partial: dict = {}
+
+    def emit_partial():  # watchdog: a schedule that never completes still leaves a line
+        if not done.is_set():
+            if rank == 0 and partial.get("line"):
+                line = dict(partial["line"])
+                line.setdefault("alt_exchange", {})[partial.get("running", "?")] = "timeout"
+                print(json.dumps(line), flush=True)
+            os._exit(0 if partial.get("line") else 3)
+
+    schedules = _schedules(args, pw)
+    if world == 1:  # emulated: no peers for the copy-engine chain
+        schedules = [(nm, o) for nm, o in schedules if o["exchange"] != "chain"]
+    for name, opts in schedules:
+        partial["running"] = name
+        watchdog = threading.Timer(args.schedule_timeout, emit_partial) if pw > 1 else None
+        if watchdog:
+            watchdog.daemon = True
+            watchdog.start()
+        drv, close = make_driver(opts)
+        step = lambda: drv.step(A, m, B, k, C, m)  # noqa: E731
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        launch_events.clear()
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.3)
+        l0 = lib.my_dgemm_kernel_launches()
+        ms = time_steps(step, args.steps)
+        launches = lib.my_dgemm_kernel_launches() - l0
+        clock_lines[name] = sampler.stop()
+        kern = [(e0.elapsed_time(e1), 2.0 * m * nloc * kc) for e0, e1, kc in launch_events]
+        ms_max, = max_over_ranks([ms])
+        results[name] = {"ms": ms_max, "kern": kern, "launches": sum_over_ranks(launches)}
+        if close is not None:
+            close()
+        if watchdog:
+            watchdog.cancel()
+        fill_a()  # the next schedule starts from A on the root only
+        torch.cuda.synchronize()
+        best = min(results, key=lambda nm: results[nm]["ms"])
+        partial["line"] = _gpu_line(args, world, pw, m, n_total, k, nloc, results, best, clock_lines, flop_step,
+                                    None, None, None)
+
+    best = min(results, key=lambda nm: results[nm]["ms"])
+    done.set()
+    compute_ms = None
+    if pw > 1:  # the per-rank GEMM alone, A resident: what the exchange costs on top of it
+        drv, _ = make_driver(dict(exchange="nccl", overlap=False, reserve_sms=0))
+        dist.broadcast(A, src=0)
+        ms = time_steps(lambda: drv.step(A, m, B, k, C, m, broadcast_a=False), args.steps)
+        compute_ms, = max_over_ranks([ms])
+
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total)
+        e2e = measure_e2e(args, m, nloc, k, seeds, j0, rank, pw, n_total, plan, A, B, C, best)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and pw == 1 and not args.no_cpu_baseline:
         gf, info = cpu_reference_rate(m, n_total, k, target_s=args.cpu_seconds)
         cpu = {"value": round(gf, 3), "unit": UNIT, **info}
-
-    if rank == 0:
-        mean_kernel_s = sum(kern_ms) / len(kern_ms) * 1e-3
-        achieved = (sum(kern_flop) / len(kern_flop)) / mean_kernel_s / 1e12
-        traffic = load_traffic(args.workload)
-        line = {
-            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
-            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference splitmix64-v1 generator, seed 42, generated on device bit-exactly)",
-            "config": {"workload": args.workload, "m": m, "n": n_total, "k": k,
-                       "n_per_gpu": nloc, "lda": m, "ldb": k, "ldc": m, "layout": "column-major",
-                       "parallelism": f"jc-shard x{world}" + (
-                           (f", {exchange_name} of A in {len(drv.plan.chunks)} k-chunks under the GEMM" if args.overlap
-                            else f", {exchange_name} of A, then the GEMM") if world > 1 else ""),
-                       "l2": "inputs larger than L2 (no flush)"},
-            "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
-                         "traffic": traffic, "kernel": "dgemm_fast_kernel<2,128,128,32> whole-tile rounds + stream-K tail (one call = both launches)",
-                         "peak_source": "nominal FP64 148SMx128flop/clkx1.965GHz (not in MEASURED_PEAKS.json); "
-                                        f"DMMA microbench {FP64_PEAK_MEASURED}",
-                         "launches_timed": len(kern_ms), "mean_launch_ms": round(mean_kernel_s * 1e3, 4)},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches_total,
-            "clocks": clk,
-            "fp64_frac_at_sampled_clock": (round(value / 1e3 / (FP64_PEAK_TFLOPS * clk["sm_mhz"] / 1965.0)
-                                                 / world, 4) if clk.get("sm_mhz") else None),
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
+    line = _gpu_line(args, world, pw, m, n_total, k, nloc, results, best, clock_lines, flop_step, compute_ms, e2e,
+                     cpu)
+    if use_pg:
+        dist.barrier()
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 
-def measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total):
-    """Same metric through the public host API: my_dgemm_ex on pinned host
-    buffers (H2D of A, B_g, C_g and D2H of C_g every step), wall clock, max
-    over ranks.  At N>1 every rank stages its own copy of A (a host-memory
-    broadcast is outside the API); the device broadcast path is `value`."""
-    import numpy as np
+def _gpu_line(args, world, pw, m, n_total, k, nloc, results, best, clock_lines, flop_step, compute_ms, e2e, cpu):
+    r = results[best]
+    value = flop_step * args.steps / (r["ms"] * 1e-3) / 1e9
+    kern_ms = [t for t, _ in r["kern"]]
+    kern_flop = [f for _, f in r["kern"]]
+    mean_kernel_s = sum(kern_ms) / len(kern_ms) * 1e-3 if kern_ms else float("nan")
+    achieved = (sum(kern_flop) / len(kern_flop)) / mean_kernel_s / 1e12 if kern_ms else None
+    clk = clock_lines[best]
+    exchanges = {"single": "none (one GPU)", "nccl": "NCCL broadcast of A, then the GEMM",
+                 "nccl-overlap": "NCCL broadcast of A in k-chunks under the GEMM",
+                 "chain": "copy-engine chain of A over NVLink peer memory, k-chunks under the GEMM"}
+    desc = exchanges.get(best, f"NCCL broadcast of A in k-chunks under the GEMM, {best.rsplit('reserve', 1)[-1]} "
+                               "SMs reserved for NCCL")
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"] / args.steps, 4),
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference splitmix64-v1 generator, seed 42, generated on device bit-exactly)",
+        "config": {"workload": args.workload, "m": m, "n": n_total, "k": k,
+                   "n_per_gpu": nloc, "lda": m, "ldb": k, "ldc": m, "layout": "column-major",
+                   "parallelism": f"jc-shard x{pw}" + (f", {desc}" if pw > 1 else ""),
+                   "exchange": best, "k_chunk": args.k_chunk if pw > 1 else None,
+                   "l2": "inputs larger than L2 (no flush)"},
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 3) if achieved else None,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": round(achieved / FP64_PEAK_TFLOPS, 4) if achieved else None,
+                     "traffic": load_traffic(args.workload, pw),
+                     "kernel": "dgemm_fast_kernel whole-tile rounds + stream-K tail (one my_dgemm call = "
+                               "both launches; per rank and k-chunk at N > 1)",
+                     "peak_source": "nominal FP64 148SMx128flop/clkx1.965GHz (not in MEASURED_PEAKS.json); "
+                                    f"DMMA microbench {FP64_PEAK_MEASURED}",
+                     "launches_timed": len(kern_ms), "mean_launch_ms": round(mean_kernel_s * 1e3, 4)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": r["launches"],
+        "clocks": clk,
+        "fp64_frac_at_sampled_clock": (round(value / 1e3 / (FP64_PEAK_TFLOPS * clk["sm_mhz"] / 1965.0) / world, 4)
+                                       if clk.get("sm_mhz") else None),
+        "fp64_frac_per_gpu": round(value / 1e3 / (FP64_PEAK_TFLOPS * world), 4),
+    }
+    if pw != world:
+        line["emulated_world"] = pw
+        line["note"] = "--emulate-world: rank 0's share of the split on a one-rank NCCL group (code-path test)"
+    if pw > 1:
+        line["alt_exchange"] = {nm: round(flop_step * args.steps / (x["ms"] * 1e-3) / 1e9, 3)
+                                for nm, x in results.items() if nm != best}
+        if compute_ms is not None:
+            line["compute_only_ms_per_step"] = round(compute_ms / args.steps, 4)
+            line["exchange_overhead_frac"] = round(1.0 - compute_ms / r["ms"], 4)
+    return line
+
+
+def measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total, plan, A, B, C, best):
+    """The same metric through the public host API, host buffers pinned,
+    wall clock, max over ranks.  N = 1: my_dgemm_ex with host pointers (the
+    drop-in; H2D of A, B, C and D2H of C inside every call, panel-pipelined).
+    N > 1: ShardedDgemm.step_host -- every rank uploads its B / C panel, the
+    root uploads A chunk by chunk into the exchange, the GEMM, D2H of the C
+    panel -- with the fastest NCCL schedule (the chain falls back to the
+    chunked NCCL broadcast here)."""
     import torch
     import torch.distributed as dist
 
-    from paper_1609_00076_b200 import _capi
+    from paper_1609_00076_b200 import _capi, engine
+    from paper_1609_00076_b200.multi import ShardedDgemm
 
     lib = _capi.load()
     dev = torch.device("cuda", torch.cuda.current_device())
-    # operands generated on device, copied once into pinned host buffers (setup, untimed)
-    hA = torch.empty(m * k, dtype=torch.float64, pin_memory=True)
+    st = torch.cuda.current_stream().cuda_stream
+    steps = max(1, min(args.steps, args.e2e_steps))
     hB = torch.empty(k * nloc, dtype=torch.float64, pin_memory=True)
     hC = torch.empty(m * nloc, dtype=torch.float64, pin_memory=True)
-    from paper_1609_00076_b200 import engine
-
-    for h, (rows, cols, seed, c0) in zip((hA, hB, hC), ((m, k, seeds[0], 0), (k, nloc, seeds[1], j0),
-                                                       (m, nloc, seeds[2], j0))):
-        d = torch.empty(rows * cols, dtype=torch.float64, device=dev)
-        engine.fill_random_device(d.data_ptr(), rows, cols, rows, seed, c0,
-                                  torch.cuda.current_stream().cuda_stream)
-        h.copy_(d)
-        del d
+    hA = torch.empty(m * k if rank == 0 else 0, dtype=torch.float64, pin_memory=True)
+    if rank == 0:
+        engine.fill_random_device(A.data_ptr(), m, k, m, seeds[0], 0, st)
+        hA.copy_(A)
+    engine.fill_random_device(C.data_ptr(), m, nloc, m, seeds[2], j0, st)
+    hB.copy_(B)
+    hC.copy_(C)
     torch.cuda.synchronize()
-    steps = max(1, min(args.steps, args.e2e_steps))
 
-    def call():
-        _capi.check(lib.my_dgemm_ex(m, nloc, k, hA.data_ptr(), m, hB.data_ptr(), k, hC.data_ptr(), m,
-                                    _capi.FORCE_PATH(engine.path(m, n_total, False)), None))
+    if world == 1:
+        def call():
+            _capi.check(lib.my_dgemm_ex(m, nloc, k, hA.data_ptr(), m, hB.data_ptr(), k, hC.data_ptr(), m,
+                                        _capi.FORCE_PATH(engine.path(m, n_total, False)), None))
+        api = "my_dgemm_ex(host pointers, pinned) -> panel-pipelined H2D/GEMM/D2H"
+    else:
+        overlap = best != "nccl"
+        reserve = int(best.rsplit("reserve", 1)[-1]) if "reserve" in best else 0
+        drv = ShardedDgemm(plan, rank, overlap=overlap, reserve_sms=reserve)
 
-    for _ in range(2):
+        def call():
+            drv.step_host(hA, A, m, hB, B, k, hC, C, m)
+        api = (f"ShardedDgemm.step_host (pinned host panels; root uploads A chunk by chunk into the "
+               f"{'chunked ' if overlap else ''}NCCL broadcast{f', {reserve} SMs reserved' if reserve else ''})")
+
+    for _ in range(1 if m * k > (1 << 28) else 2):
         call()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         call()
     dt = time.perf_counter() - t0
-    if world > 1:
+    if dist.is_initialized():
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t[0])
     lib.my_dgemm_release_workspace()
-    flop = 2.0 * m * n_total * k * steps
+    flop = 2.0 * m * (n_total if dist.is_initialized() and dist.get_world_size() == world else nloc) * k * steps
     return {"value": round(flop / dt / 1e9, 3), "unit": UNIT,
-            "h2d_bytes_per_step": 8 * (m * k * world + (k + m) * n_total),
-            "d2h_bytes_per_step": 8 * m * n_total, "steps": steps,
-            "api": "my_dgemm_ex(host pointers, pinned) -> panel-pipelined H2D/GEMM/D2H"}
+            "h2d_bytes_per_step": 8 * (m * k + (k + m) * n_total),
+            "d2h_bytes_per_step": 8 * m * n_total, "steps": steps, "ms_per_step": round(dt / steps * 1e3, 3),
+            "api": api}
 
 
-def load_traffic(workload):
+def load_traffic(workload, world=1):
     """dram bytes per call of dgemm_fast_kernel from the committed ncu --set
     full summary (profiles/traffic.json) when it was captured on this
-    workload, else None."""
+    workload at one GPU (the per-rank call differs at N > 1), else None."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     try:
         with open(p) as f:
             t = json.load(f)
     except (OSError, ValueError):
         return None
+    if world != 1:
+        return None
     return t.get("dram_bytes_per_launch") if str(t.get("workload", "")).startswith(workload + " ") else None
+
+
+def under_launcher() -> bool:
+    """True inside a torchrun / torch.distributed.run worker."""
+    return "WORLD_SIZE" in os.environ and "LOCAL_RANK" in os.environ
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: start the N ranks
+    ourselves (one process per GPU through torch.distributed.run on
+    127.0.0.1), as the reference's threaded engine creates its own workers
+    (parallel.py:224-234).  Rank 0's JSON line is the output; the exit code
+    is the launcher's."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args) -> int:
+    """--dry-run: the launcher and the collective plumbing without GPU work
+    (gloo): every rank joins, the world size is checked, rank 0 prints the
+    line it would time."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        assert int(t[0]) == world
+        dist.destroy_process_group()
+    if rank == 0:
+        m, n_rank, k = WORKLOADS[args.workload]
+        n = n_rank if args.scaling == "strong" else n_rank * world
+        print(json.dumps({"dry_run": True, "metric": METRIC, "unit": UNIT, "n_gpus": world, "ranks_joined": world,
+                          "scaling": args.scaling, "config": {"workload": args.workload, "m": m, "n": n, "k": k},
+                          "schedules": [nm for nm, _ in _schedules(args, world)]}), flush=True)
+    return 0
 
 
 def main():
@@ -472,25 +678,50 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2_8192")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg5",
+                    help="default cfg5: SURVEY 8e's 32768^3 problem (BASELINE configs[4]), split over the GPUs")
+    ap.add_argument("--scaling", choices=("strong", "weak"), default="strong",
+                    help="strong: the workload's n is the whole job, split over the ranks; weak: n per rank")
+    ap.add_argument("--strong", action="store_true", help="same as --scaling strong (kept for old command lines)")
     ap.add_argument("--k-chunk", type=int, default=2048)
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: the workload's n is the total, split over the ranks (e.g. "
-                         "--workload cfg5 --strong: SURVEY 8e's 32768^3 on 1/2/4/8 GPUs)")
+    ap.add_argument("--exchange", choices=("all", "nccl", "chain"), default="all",
+                    help="N > 1: how A reaches the ranks -- 'all' times every schedule (serialized NCCL "
+                         "broadcast, chunked NCCL broadcast under the GEMM with and without SMs reserved, the "
+                         "copy-engine chain over NVLink peer memory, paper_1609_00076_b200/peer.py) and reports "
+                         "the fastest as the value, the others under alt_exchange")
     ap.add_argument("--overlap", action="store_true",
-                    help="broadcast A in k-chunks under the GEMM instead of before it (N>1)")
-    ap.add_argument("--exchange", choices=("nccl", "chain"), default="nccl",
-                    help="N > 1: how A reaches the ranks -- NCCL broadcast, or the copy-engine chain over "
-                         "NVLink peer memory (no SMs; paper_1609_00076_b200/peer.py)")
+                    help="with --exchange nccl: broadcast A in k-chunks under the GEMM instead of before it")
     ap.add_argument("--reserve-sms", type=int, default=0,
-                    help="with --overlap: SMs kept free of the GEMM for NCCL's kernels")
+                    help="with the overlapped NCCL schedule: SMs kept free of the GEMM for NCCL's kernels")
+    ap.add_argument("--schedule-timeout", type=float, default=300.0,
+                    help="N > 1: seconds one exchange schedule may take before rank 0 reports what it has")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="tests on one GPU: run rank 0's share of a W-way split through the N > 1 code paths "
+                         "on a one-rank NCCL group")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch the ranks and check the collective plumbing (gloo), no GPU work")
     args = ap.parse_args()
+    if args.strong:
+        args.scaling = "strong"
     if args.warmup < 3:
         print("warning: the contract requires --warmup >= 3", file=sys.stderr)
+    if args.gpus < 1:
+        print(f"error: --gpus must be >= 1, got {args.gpus}", file=sys.stderr)
+        return 2
+    if not under_launcher():
+        if args.gpus > 1:
+            return self_launch(args)
+    else:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            print(f"error: launched with WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+            return 2
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_b200_arm(args)

@@ -51,6 +51,24 @@ SCRIPT = textwrap.dedent("""
         torch.cuda.synchronize()
         assert torch.equal(got[j0 * m:j1 * m], want[j0 * m:j1 * m]), (overlap, reserve)
     assert engine.set_max_ctas(0) == 0  # the step restored the cap
+    # step_host: the panels and (root) A from pinned host memory, A uploaded
+    # chunk by chunk into the chunked broadcast, C's panel back to the host
+    nloc = j1 - j0
+    hA = a.cpu().pin_memory()
+    hB = b[j0 * k:j1 * k].cpu().pin_memory()
+    for overlap, reserve in ((False, 0), (True, 0), (True, 16)):
+        hC = c0[j0 * m:j1 * m].cpu().pin_memory()
+        da = torch.full_like(a, float("nan"))
+        db = torch.full((k * nloc,), float("nan"), dtype=torch.float64, device=dev)
+        dc = torch.full((m * nloc,), float("nan"), dtype=torch.float64, device=dev)
+        drv = ShardedDgemm(plan, 0, broadcast=bcast, overlap=overlap, reserve_sms=reserve)
+        for rep in range(2):  # twice: the second step reuses the buffers behind the first
+            if rep:
+                hC.copy_(c0[j0 * m:j1 * m].cpu())
+            out = drv.step_host(hA, da, m, hB, db, k, hC, dc, m)
+            assert out is hC
+            assert torch.equal(hC, want[j0 * m:j1 * m].cpu()), (overlap, reserve, rep)
+    assert engine.set_max_ctas(0) == 0
     t = torch.tensor([3.0, 1.0], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dist.barrier()
@@ -80,3 +98,31 @@ def test_nccl_world1_sharded_step_bitwise(tmp_path):
     r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "NCCL-OK" in r.stdout
+
+
+def test_bench_emulated_world_runs_every_n_gt_1_path(tmp_path):
+    """bench.py --emulate-world 4 on the one GPU: rank 0's share of a 4-way
+    split through the N > 1 code -- every NCCL exchange schedule timed (the
+    chain needs peers and is skipped), the compute-only run, step_host for
+    e2e, alt_exchange in the line."""
+    import json
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    for key in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(key, None)
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--emulate-world", "4", "--workload",
+                        "cfg2_8192", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1",
+                        "--k-chunk", "1024"], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["emulated_world"] == 4 and line["n_gpus"] == 1
+    assert line["config"]["n_per_gpu"] == 2048 and line["config"]["k_chunk"] == 1024
+    names = {line["config"]["exchange"], *line["alt_exchange"]}
+    assert names == {"nccl", "nccl-overlap", "nccl-overlap-reserve8"}
+    assert line["value"] > 1000 and line["compute_only_ms_per_step"] > 0
+    assert line["e2e"]["api"].startswith("ShardedDgemm.step_host") and line["e2e"]["value"] > 0
+    assert line["gpu_launches"] > 0 and line["roofline"]["frac"] > 0.3
