@@ -285,6 +285,7 @@ def run_reference_arm(args):
                            "problem (cpu_baseline.sample)"},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, **info},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms": [round(t * 1e3, 1) for t in times],
     }
     print(json.dumps(line), flush=True)
     return 0
