@@ -87,6 +87,30 @@ MYD_DEVICE void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, u
       : "memory");
 }
 
+// The same with an L2 eviction-priority hint (a createpolicy value).
+MYD_DEVICE void bulk_g2s_hint(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+MYD_DEVICE uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+MYD_DEVICE uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+MYD_DEVICE uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+
 // Bulk (TMA-engine) copy shared -> global, tracked in this thread's bulk
 // group; same alignment rules.  Generic-proxy writes to the source must be
 // made visible first (fence_proxy_async_smem by the writing threads).

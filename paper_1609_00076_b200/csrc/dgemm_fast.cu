@@ -98,6 +98,10 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_CGLOBAL
 #define MYD_CGLOBAL 1  // full 128x128 tiles read C from global memory (0: through the ring, for A/B timing)
 #endif
+#ifndef MYD_L2_HINTS
+#define MYD_L2_HINTS 0  // 1: A slabs evict_last, B slabs evict_first (full tiles); 2: the reverse;
+                        // 3: A evict_last only; 4: B evict_first only (profiles/r02/l2_hints_r02*.log)
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -376,6 +380,20 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if (blockIdx.x == 0 && pw == 0 && lane == 0) g_tl[8] = gtimer();
 #endif
     uint32_t g = 0;  // ring slots filled by this CTA so far (C blocks and slabs)
+    [[maybe_unused]] uint64_t pol_a = 0, pol_b = 0;
+    if constexpr (MYD_L2_HINTS == 1) {
+      pol_a = l2_policy_evict_last();
+      pol_b = l2_policy_evict_first();
+    } else if constexpr (MYD_L2_HINTS == 2) {
+      pol_a = l2_policy_evict_first();
+      pol_b = l2_policy_evict_last();
+    } else if constexpr (MYD_L2_HINTS == 3) {
+      pol_a = l2_policy_evict_last();
+      pol_b = l2_policy_evict_normal();
+    } else if constexpr (MYD_L2_HINTS == 4) {
+      pol_a = l2_policy_evict_normal();
+      pol_b = l2_policy_evict_first();
+    }
     int cur = seg_first();
     Seg sg;
     bool have = seg_at(cur, sg);  // integer work, overlapping the previous grid's drain
@@ -469,13 +487,26 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
           if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
           __syncwarp();
-          if (lane < A_ROWS) {
-            const int kk = pw * A_ROWS + lane;
-            bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
-          }
-          if (lane < RW) {
-            const int nn = pw * RW + lane;
-            bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+          if constexpr (MYD_L2_HINTS != 0 && BM == 128 && BN == 128) {
+            // raster bands share A panels across waves (GROUP_M tile rows) and
+            // B panels within a wave: keep the band's A (or B) in L2
+            if (lane < A_ROWS) {
+              const int kk = pw * A_ROWS + lane;
+              bulk_g2s_hint(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot], pol_a);
+            }
+            if (lane < RW) {
+              const int nn = pw * RW + lane;
+              bulk_g2s_hint(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot], pol_b);
+            }
+          } else {
+            if (lane < A_ROWS) {
+              const int kk = pw * A_ROWS + lane;
+              bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, BM * 8, &full_bar[slot]);
+            }
+            if (lane < RW) {
+              const int nn = pw * RW + lane;
+              bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+            }
           }
 #ifdef MYD_TIMELINE
           if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg && kt == sg.kb) g_tl[7] = gtimer();
