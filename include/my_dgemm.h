@@ -53,6 +53,12 @@ extern "C" {
 #define MY_DGEMM_BLAS_EPILOGUE 0x1000u /* my_dgemm_blas (tests): apply alpha / beta in the kernel epilogue
                                           instead of the reference-BLAS order (C := beta C, alpha folded
                                           into an operand, then the contract) that large tiled calls use */
+#define MY_DGEMM_FORCE_SMALL 0x2000u /* tiled path on the small-block kernel (tests, tuner); variant below */
+/* Small-block kernel variant v (1..10, block / slab / ring shapes listed in
+ * csrc/dgemm_small.cu; 0: the cheapest by the planner's model), with
+ * MY_DGEMM_FORCE_SMALL. */
+#define MY_DGEMM_SMALL_VARIANT(v) ((unsigned)(v) << 14)
+#define MY_DGEMM_SMALL_MASK 0x3C000u
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The

@@ -7,8 +7,9 @@
  * timed CPU baseline.  The product path (paper_1609_00076_b200) never links,
  * imports or executes this file.
  *
- * Parity is pinned: oracle/pin_golden.py compares every function here with
- * the reference package (/root/reference/pkg, imported in the build
+ * Parity is pinned: tests/golden/make_golden.py (which writes the fixtures)
+ * and tests/test_oracle.py compare every function here with the reference
+ * package (/root/reference/pkg, imported in the build
  * container) and with the reference tests' own golden values
  * (pkg/tests/test_matrix.py:42-52 GOLDEN_SEED42), and the resulting fixtures
  * are committed under tests/golden/.

@@ -25,6 +25,13 @@ FORCE_UNITS8 = 0x40
 FORCE_ROWS16 = 0x80
 FORCE_STREAMK = 0x800
 BLAS_EPILOGUE = 0x1000
+FORCE_SMALL = 0x2000
+
+
+def SMALL_VARIANT(v: int) -> int:  # noqa: N802 - mirrors the C macro
+    return v << 14
+
+
 IPC_HANDLE_BYTES = 64
 PATH_TILED, PATH_GEMV_N1, PATH_GEMV_M1, PATH_FEW_COLS, PATH_FEW_ROWS, PATH_EXACT, PATH_ROWS_DMMA = range(7)
 

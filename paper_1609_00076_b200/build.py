@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmy_dgemm_b200.so")
-SOURCES = ["dgemm_fast.cu", "dgemm_skinny.cu", "dgemm_aux.cu", "blas.cu", "level3.cu", "host_path.cu", "multi_host.cu", "tune.cu", "peer.cu", "capi.cu"]
+SOURCES = ["dgemm_fast.cu", "dgemm_small.cu", "dgemm_skinny.cu", "dgemm_aux.cu", "blas.cu", "level3.cu", "host_path.cu", "multi_host.cu", "tune.cu", "peer.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1118,6 +1118,11 @@ int set_max_ctas(int n) { return g_max_ctas.exchange(n); }
 // units.  force_split pins the plan (tests and the tuner): 0 = heuristic,
 // 1 = full tiles only, 2 / 4 / 8 / 16 = every tile as 128x64 / 128x32 /
 // 64x32 / 16x128 units.  Every plan computes bitwise the same C.
+double small_cost_us(int v, int M, int N, int K, int G);  // dgemm_small.cu
+int small_variants();
+cudaError_t launch_dgemm_small(int variant, int M, int N, int K, const double *A, int64_t lda, const double *B,
+                               int64_t ldb, double *C, int64_t ldc, cudaStream_t st, const Epilogue &ep, bool vec2);
+
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -1134,8 +1139,11 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   int split = 1;            // 1 full tiles; 2 / 4 / 8 units 128x64 / 128x32 / 64x32; 16 units 16x128
   auto per_tile = [](int s) { return s == 16 ? 8 : s; };
   int sk_split = force_split >= 32 ? (force_split == 32 ? 1 : force_split - 32) : 1;  // stream-K unit shape
-  bool streamk = force_split >= 32 && tiles * sk_split >= G;
-  if (force_split >= 32) {
+  bool streamk = force_split >= 32 && force_split < 64 && tiles * sk_split >= G;
+  double plan_best = 1e300;  // the heuristic's cost of its persistent-kernel plan (us)
+  if (force_split >= 64) {
+    q = tiles;  // small-block kernel, below
+  } else if (force_split >= 32) {
     q = tiles;  // (fewer units than SMs: plain full tiles instead)
   } else if (force_split > 1) {
     split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
@@ -1257,15 +1265,39 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         }
       }
     }
+    plan_best = best;
+  }
+  // Small-block kernel (dgemm_small.cu): below a few waves of units, CTAs
+  // of 16x16 .. 64x64 blocks with several per SM beat the persistent grid's
+  // few long unit chains; bitwise the same C.  force_split 64 + v pins
+  // variant v (64: the cheapest variant by the model).
+  int small_v = 0;
+  if (force_split >= 64) {
+    small_v = force_split - 64;
+    if (small_v == 0) {
+      double sbest = 1e300;
+      for (int v = 1; v <= small_variants(); ++v) {
+        const double c = small_cost_us(v, M, N, K, (int)G);
+        if (c < sbest) sbest = c, small_v = v;
+      }
+    }
+  } else if (force_split == 0 && tiles <= 2 * G) {
+    double sbest = plan_best;
+    for (int v = 1; v <= small_variants(); ++v) {
+      const double c = small_cost_us(v, M, N, K, (int)G);
+      if (c < sbest - 1e-9) sbest = c, small_v = v;
+    }
   }
   static const bool trace = [] {  // MY_DGEMM_PLAN_TRACE=1: print each call's launch plan to stderr
     const char *v = getenv("MY_DGEMM_PLAN_TRACE");
     return v && *v && *v != '0';
   }();
   if (trace)
-    fprintf(stderr, "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d q=%lld raster=%dx%d edge=%d\n",
-            M, N, K, (long long)tiles_m, tiles_n, streamk ? "stream-K" : "units", split, sk_split, q, raster_m,
-            raster_n, edge);
+    fprintf(stderr,
+            "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d q=%lld raster=%dx%d edge=%d small=%d\n",
+            M, N, K, (long long)tiles_m, tiles_n, small_v ? "small" : (streamk ? "stream-K" : "units"), split, sk_split, q,
+            raster_m, raster_n, edge, small_v);
+  if (small_v > 0) return launch_dgemm_small(small_v, M, N, K, A, lda, B, ldb, C, ldc, stream, ep, vec2);
   if (streamk) {
     SkWorkspace ws;
     cudaError_t e = ws.alloc((int)G, stream);

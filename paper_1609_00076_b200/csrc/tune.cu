@@ -74,8 +74,12 @@ extern "C" int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int
     if ((e = launch_fill_random(B, k, n, ldb, 2, 0, st)) != cudaSuccess) break;
     if ((e = launch_fill_random(C, m, n, ldc, 3, 0, st)) != cudaSuccess) break;
     if ((e = cudaEventCreate(&e0)) != cudaSuccess || (e = cudaEventCreate(&e1)) != cudaSuccess) break;
-    const int plans[] = {0, 1, 2, 4, 8, 16, 32, 34, 36, 40};
+    // small-block kernel variants (plans 65..74) for problems up to a few
+    // waves of tiles; larger problems skip them (each would take minutes)
+    const long long tiles = (long long)((m + 127) / 128) * ((n + 127) / 128);
+    const int plans[] = {0, 1, 2, 4, 8, 16, 32, 34, 36, 40, 65, 66, 67, 68, 69, 70, 71, 72, 73, 74};
     for (int plan : plans) {
+      if (plan >= 64 && tiles > 4 * 148) continue;
       const Epilogue ep{};
       if ((e = launch_dgemm_fast(m, n, k, A, lda, B, ldb, C, ldc, st, false, plan, ep)) != cudaSuccess) break;
       cudaEventRecord(e0, st);

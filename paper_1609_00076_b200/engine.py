@@ -145,7 +145,8 @@ def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, str
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
     f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
           16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
-          36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8}[strips]
+          36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
+          **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(11)}}[strips]
     return f
 
 
@@ -247,7 +248,8 @@ def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int
     """Raw device-pointer call (asynchronous on `stream`).  `strips` pins
     the launch plan (tests, tuning): 2 / 4 / 8 / 16 every tile as 128x64 /
     128x32 / 64x32 / 16x128 units, 32 / 34 / 36 / 40 the stream-K schedule
-    over full tiles / those units; `path` forces a kernel family
+    over full tiles / those units, 64 + v the small-block kernel's variant v
+    (1..10; 64: the planner's pick); `path` forces a kernel family
     (_capi.PATH_*, what sharded drivers pass to every shard).  Every plan
     gives bitwise the same C."""
     lib = _capi.load()

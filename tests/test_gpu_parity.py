@@ -288,7 +288,7 @@ def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     sequence does not depend on the CTA shape or on who runs which slabs)."""
     a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
     outs = []
-    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40):
+    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40) + SMALL_PLANS:
         cc = c.clone()
         run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips)
         outs.append(cc)
@@ -300,6 +300,41 @@ def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
     host = outs[3].cpu().numpy()
     if ldc > m:
         assert np.all(host.reshape(n, ldc)[:, m:] == -777.25)
+
+
+SMALL_PLANS = tuple(range(64, 75))  # the small-block kernel: planner's pick, then variants 1..10
+
+
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (256, 256, 256, 256, 256, 256),      # the sub-wave point of the cfg2 sweep
+    (37, 53, 71, 44, 76, 40),            # cfg3d: ragged everything, odd lds (8-byte staging)
+    (17, 17, 4096, 17, 4096, 17),        # tiny m x n, long K chain
+    (129, 65, 33, 130, 34, 131),         # one past a block in m and n, K one past a slab, odd ldc
+    (200, 300, 1000, 200, 1000, 200),    # ragged K (1000 = 31 slabs of 32 + 8)
+    (512, 512, 513, 512, 514, 512),      # K one past a 4-group: the zero-filled tail group
+    (64, 64, 2, 64, 2, 64),              # K < 4
+    (1000, 1000, 64, 1001, 65, 1002),    # short K, odd lds, many blocks
+])
+def test_small_kernel_bitwise_equals_units(torch_cuda, m, n, k, lda, ldb, ldc):
+    """The small-block kernel (csrc/dgemm_small.cu) is one more plan of the
+    tiled path: every variant gives bitwise the C of the persistent kernel's
+    64x32-unit plan (same DMMA chain per element), never writes padding
+    rows, and is within the headline bound of the exact kernel."""
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
+    ref = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ref, ldc, strips=8, force_tiled=True)
+    for strips in SMALL_PLANS:
+        for vec1 in (False, True):
+            cc = c.clone()
+            run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True,
+                    force_vec1=vec1)
+            assert torch_cuda.equal(cc, ref), (strips, vec1)
+    ce = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch_cuda, m, n, k, ref, ce, ldc, bound)
+    if ldc > m:
+        assert np.all(ref.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
 
 
 def test_fast_deterministic(torch_cuda):
@@ -1046,7 +1081,7 @@ def test_signed_zero_is_plan_invariant_and_matches_the_oracle(torch_cuda, m, n, 
     ce = c.clone()
     run_dev(torch, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
     assert bool(torch.signbit(ce.view(n, ldc)[:, :m]).all())
-    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40):
+    for strips in (0, 2, 4, 8, 16, 32, 34, 36, 40) + SMALL_PLANS:
         cc = c.clone()
         run_dev(torch, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips, force_tiled=True)
         assert bool(torch.signbit(cc.view(n, ldc)[:, :m]).all()), strips
