@@ -59,6 +59,7 @@ extern "C" {
  * MY_DGEMM_FORCE_SMALL. */
 #define MY_DGEMM_SMALL_VARIANT(v) ((unsigned)(v) << 14)
 #define MY_DGEMM_SMALL_MASK 0x3C000u
+#define MY_DGEMM_FORCE_TILES 0x40000u /* every tile as a full 128x128 tile (tests, tuner: plan 1) */
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The
@@ -206,6 +207,20 @@ MY_DGEMM_API int my_dgemm_diff_report(int64_t m, int64_t n, const double *X, int
  * 128x64 / 128x32 / 64x32 units.
  */
 MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int reps, int *out_plan, double *out_ms);
+/*
+ * Tile parameters of launch plan `plan` (my_dgemm_tune's plan ids, plus
+ * 65..74 = the small-block kernel's variants 1..10) at depth k: the CTA block
+ * bm x bn, the K-slab depth bk and the shared-memory ring depth stages, as
+ * compiled (vec2 != 0: 16-byte operand staging).  These are the GPU's blocking
+ * parameters (the reference's mc / nc / kc, Config.goto, config.py:24-40);
+ * engine.tune_grid searches them like the reference's tune()
+ * (pkg/src/gemmforge/bench.py:238-311).  Returns 0, or -1 for an unknown plan.
+ */
+MY_DGEMM_API int my_dgemm_plan_geometry(int plan, int k, int vec2, int *bm, int *bn, int *bk, int *stages);
+/* Pin `plan` for later calls of this shape and operand alignment (what
+ * my_dgemm_tune records; engine.tune_grid's winner).  Negative status for a
+ * bad argument or an unknown plan. */
+MY_DGEMM_API int my_dgemm_tune_set(int m, int n, int k, int lda, int ldb, int plan);
 MY_DGEMM_API void my_dgemm_tune_clear(void);
 
 /*

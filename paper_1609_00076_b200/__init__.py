@@ -31,5 +31,6 @@ from .engine import (  # noqa: F401
     register,
     tune,
 )
+from .tuning import TilePoint, TileTuneResult, tune_grid  # noqa: F401
 
 __version__ = "0.1.0"

@@ -26,6 +26,7 @@ FORCE_ROWS16 = 0x80
 FORCE_STREAMK = 0x800
 BLAS_EPILOGUE = 0x1000
 FORCE_SMALL = 0x2000
+FORCE_TILES = 0x40000
 
 
 def SMALL_VARIANT(v: int) -> int:  # noqa: N802 - mirrors the C macro
@@ -67,6 +68,9 @@ SIGNATURES = {
                                   ctypes.POINTER(_I64), ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
     "my_dgemm_tune": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_D)]),
     "my_dgemm_tune_clear": (None, []),
+    "my_dgemm_plan_geometry": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),
+                                    ctypes.POINTER(_I)]),
+    "my_dgemm_tune_set": (_I, [_I, _I, _I, _I, _I, _I]),
     "my_dgemm_set_max_ctas": (_I, [_I]),
     "my_dgemm_path": (_I, [_I, _I, ctypes.c_uint]),
     "my_dgemm_ipc_export": (_I, [_P, ctypes.c_char_p, ctypes.POINTER(_U64)]),

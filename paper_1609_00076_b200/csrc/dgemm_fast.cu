@@ -1349,7 +1349,51 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
                                 (int)main_tiles, edge, main_tiles > 0, stream);
 }
 
+struct SmallGeo {
+  int bm = 0, bn = 0, bk = 0, stages = 0;
+};
+SmallGeo small_geo(int v);  // dgemm_small.cu
+
+// Blocking parameters of a launch plan (my_dgemm_plan_geometry).
+bool plan_geometry(int plan, int K, bool vec2, int &bm, int &bn, int &bk, int &stages) {
+  using namespace fast;
+  if (plan >= 65) {
+    const SmallGeo g = small_geo(plan - 64);
+    bm = g.bm, bn = g.bn, bk = g.bk, stages = g.stages;
+    return g.bm != 0;
+  }
+  const int s = plan >= 32 ? (plan == 32 ? 1 : plan - 32) : (plan == 0 ? 1 : plan);
+  switch (s) {
+    case 1:
+      if (vec2 && K >= MYD_BK32_MIN_K) {
+        bm = 128, bn = 128, bk = 32, stages = Ring<128, 128, 32>::STAGES;
+      } else {
+        bm = 128, bn = 128, bk = 16, stages = Ring<128, 128, 16>::STAGES;
+      }
+      return true;
+    case 2: bm = 128, bn = 64, bk = Ring<128, 64>::BK, stages = Ring<128, 64>::STAGES; return true;
+    case 4: bm = 128, bn = 32, bk = Ring<128, 32>::BK, stages = Ring<128, 32>::STAGES; return true;
+    case 8: bm = 64, bn = 32, bk = Ring<64, 32>::BK, stages = Ring<64, 32>::STAGES; return true;
+    case 16:
+      if (plan >= 32) return false;
+      bm = 16, bn = 128, bk = MYD_ROWS16_BK, stages = Ring<16, 128, MYD_ROWS16_BK>::STAGES;
+      return true;
+    default: return false;
+  }
+}
+
 }  // namespace myd
+
+extern "C" __attribute__((visibility("default"))) int my_dgemm_plan_geometry(int plan, int k, int vec2, int *bm,
+                                                                             int *bn, int *bk, int *stages) {
+  int a = 0, b = 0, c = 0, d = 0;
+  if (!myd::plan_geometry(plan, k, vec2 != 0, a, b, c, d)) return -1;
+  if (bm) *bm = a;
+  if (bn) *bn = b;
+  if (bk) *bk = c;
+  if (stages) *stages = d;
+  return 0;
+}
 
 #ifdef MYD_TIMELINE
 extern "C" __attribute__((visibility("default"))) void my_dgemm_timeline(unsigned long long *out, int reset) {

@@ -280,7 +280,7 @@ cudaError_t launch_small_v(int variant, int M, int N, int K, const double *A, in
 
 }  // namespace
 
-struct SmallGeo {
+struct SmallGeo {  // also declared in dgemm_fast.cu
   int bm = 0, bn = 0, bk = 0, stages = 0;
 };
 // Geometry of small-kernel variant v (bm == 0: no such variant).

@@ -114,6 +114,24 @@ extern "C" int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int
   return capi_ok();
 }
 
+namespace myd {
+bool plan_geometry(int plan, int K, bool vec2, int &bm, int &bn, int &bk, int &stages);
+}
+
+extern "C" int my_dgemm_tune_set(int m, int n, int k, int lda, int ldb, int plan) {
+  if (m < 1) return capi_fail(-1, "matrix dims must be positive");
+  if (n < 1) return capi_fail(-2, "matrix dims must be positive");
+  if (k < 1) return capi_fail(-3, "matrix dims must be positive");
+  if (lda < m) return capi_fail(-4, "leading dimension lda smaller than m");
+  if (ldb < k) return capi_fail(-5, "leading dimension ldb smaller than k");
+  int bm, bn, bk, st;
+  if (plan != 0 && !plan_geometry(plan, k, true, bm, bn, bk, st))
+    return capi_fail(-6, "unknown launch plan " + std::to_string(plan));
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tuned[make_key(m, n, k, lda, ldb)] = plan;
+  return capi_ok();
+}
+
 extern "C" void my_dgemm_tune_clear(void) {
   std::lock_guard<std::mutex> lk(g_tune_mu);
   g_tuned.clear();

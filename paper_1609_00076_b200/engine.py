@@ -143,7 +143,7 @@ def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, str
     f |= _capi.FORCE_PATH(path) if path is not None else 0
     f |= _capi.FORCE_TILED if force_tiled else 0
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
-    f |= {0: 0, 1: 0, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
+    f |= {0: 0, 1: _capi.FORCE_TILES, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
           16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
           36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
           **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(11)}}[strips]
@@ -246,7 +246,7 @@ def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int
                  stream: int = 0, exact: bool = False, force_tiled: bool = False,
                  force_vec1: bool = False, strips: int = 0, path: int | None = None) -> None:
     """Raw device-pointer call (asynchronous on `stream`).  `strips` pins
-    the launch plan (tests, tuning): 2 / 4 / 8 / 16 every tile as 128x64 /
+    the launch plan (tests, tuning): 1 full tiles only, 2 / 4 / 8 / 16 every tile as 128x64 /
     128x32 / 64x32 / 16x128 units, 32 / 34 / 36 / 40 the stream-K schedule
     over full tiles / those units, 64 + v the small-block kernel's variant v
     (1..10; 64: the planner's pick); `path` forces a kernel family

@@ -253,3 +253,46 @@ def test_diagnostics_mirror_the_reference():
     assert not rep.clean
     e = engine.VerificationError("C[ 1 ][ 2 ] != C_ref, 1E0, 2E0", m=3, n=4, k=5, algorithm="b200")
     assert (e.diagnostic, e.m, e.n, e.k, e.algorithm) == ("C[ 1 ][ 2 ] != C_ref, 1E0, 2E0", 3, 4, 5, "b200")
+
+
+def test_plan_geometry_is_the_compiled_tile_table(lib):
+    """my_dgemm_plan_geometry reports every launch plan's blocking parameters
+    (no GPU needed): the persistent kernel's unit shapes and the small-block
+    kernel's variant table; unknown plans are -1."""
+    from paper_1609_00076_b200 import tuning
+
+    full_long = tuning.plan_geometry(1, 8192)
+    assert (full_long.bm, full_long.bn, full_long.bk) == (128, 128, 32) and full_long.stages >= 3
+    assert tuning.plan_geometry(1, 256).bk == 16  # short K: 16-deep slabs
+    assert tuning.plan_geometry(1, 8192, vec2=False).bk == 16
+    assert tuning.plan_geometry(36, 512).key[:2] == (128, 32)  # stream-K over 128x32 units
+    assert tuning.plan_geometry(16, 512).key[:2] == (16, 128)
+    assert tuning.plan_geometry(48, 512) is None and tuning.plan_geometry(75, 512) is None
+    small = [tuning.plan_geometry(p, 512) for p in range(65, 75)]
+    assert all(p is not None for p in small)
+    assert (small[0].bm, small[0].bn, small[0].bk, small[0].stages) == (16, 16, 32, 4)
+    for p in small + [full_long]:  # every ring fits the 227 KB opt-in shared memory
+        assert p.footprint * 8 <= 232448
+
+
+def test_tile_grid_expansion_and_tie_break(lib):
+    """tune_grid's validation (bench.py:258-272 analogue): a fully specified
+    grid point no instantiation carries is skipped with a reason, a partial
+    grid keeps every compiled plan on its axes, and exact rate ties prefer
+    the smaller footprint (bench.py:304-311)."""
+    from paper_1609_00076_b200 import tuning
+
+    pts, skipped = tuning.grid_points({"bm": [16, 32], "bn": [16], "bk": [32, 48], "stages": [4]}, 512)
+    assert {p.key for p in pts} == {(16, 16, 32, 4), (32, 16, 32, 4)}
+    assert {s[0] for s in skipped} == {(16, 16, 48, 4), (32, 16, 48, 4)}
+    assert all("no compiled instantiation" in s[1] for s in skipped)
+    pts, skipped = tuning.grid_points({"bm": [128]}, 4096)
+    assert pts and all(p.bm == 128 for p in pts) and not skipped
+    assert {p.plan for p in pts} >= {1, 2, 4, 32, 34, 36}
+    with pytest.raises(ValueError):
+        tuning.grid_points({"mc": [64]}, 512)
+    a = tuning.TilePoint(64, 64, 16, 6, 69)
+    b = tuning.TilePoint(32, 32, 32, 4, 67)
+    assert tuning._beats(10.0, b, 10.0, a)  # smaller footprint wins the tie
+    assert not tuning._beats(10.0, a, 10.0, b)
+    assert tuning._beats(10.5, a, 10.0, b)

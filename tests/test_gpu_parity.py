@@ -1210,3 +1210,33 @@ def test_cfg2_sweep_point_exact_kat_and_fast_full(torch_cuda, golden, s):
     run_dev(torch, s, s, s, a, s, b, s, exact, s, exact=True)
     assert oracle.sha256_valid(exact.cpu().numpy(), s, s, s) == kat["sha256"]
     check_dev(torch, s, s, s, fast, exact, s, bound)
+
+
+def test_tile_grid_tuner_pins_a_verified_winner(torch_cuda):
+    """tune_grid (the reference's tune, bench.py:238-311): every timed point is
+    verified against the exact kernel, blocks larger than the probe are
+    skipped with a warning, the winner is pinned for the probe shape
+    (my_dgemm_tune_set) and later calls of the shape are bitwise what the
+    heuristic plan gives."""
+    import io
+
+    from paper_1609_00076_b200 import tuning
+
+    _capi.load().my_dgemm_tune_clear()
+    log = io.StringIO()
+    try:
+        res = tuning.tune_grid({}, probe_size=96, reps=2, log=log)
+        assert res.table and res.rate > 0 and res.best in res.table
+        assert res.rate == max(res.table.values())
+        assert all(p.bm <= 96 and p.bn <= 96 for p in res.table)
+        assert "block sizes exceed probe size 96" in log.getvalue()  # the 128-row units
+        m = n = k = 96
+        a, b, c, _ = dev_operands(torch_cuda, m, n, k)
+        tuned = c.clone()
+        run_dev(torch_cuda, m, n, k, a, m, b, k, tuned, m)  # uses the pinned plan
+        _capi.load().my_dgemm_tune_clear()
+        heur = c.clone()
+        run_dev(torch_cuda, m, n, k, a, m, b, k, heur, m)
+        assert torch_cuda.equal(tuned, heur)
+    finally:
+        _capi.load().my_dgemm_tune_clear()
