@@ -60,7 +60,6 @@ extern "C" {
 #define MY_DGEMM_SMALL_VARIANT(v) ((unsigned)(v) << 14)
 #define MY_DGEMM_SMALL_MASK 0x3C000u
 #define MY_DGEMM_FORCE_TILES 0x40000u /* every tile as a full 128x128 tile (tests, tuner: plan 1) */
-#define MY_DGEMM_FORCE_TWO_GROUP 0x80000u /* 128x64 units on two phase-shifted consumer groups per CTA (plan 3) */
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The

@@ -144,7 +144,7 @@ constexpr int default_bk() {
   return (BM * BN) / (CONSUMER_WARPS * 64) >= 16 ? 16 : ((BM * BN) / (CONSUMER_WARPS * 64) >= 8 ? 32 : 64);
 }
 
-template <int BM, int BN, int BK_ = default_bk<BM, BN>(), int GRP_ = 1>
+template <int BM, int BN, int BK_ = default_bk<BM, BN>()>
 struct Ring {
   static constexpr int BK = BK_;
   static constexpr int AP = BM + 4;
@@ -161,12 +161,11 @@ struct Ring {
                              : (32 <= BN && 32 * CP <= SLOT) ? 32
                              : (16 * CP <= SLOT) ? 16 : 8;
   static constexpr int CS = BN / CPS;
-  static constexpr int STAGES_FIT = SMEM_BUDGET / GRP_ / ((A_ST + B_ST) * 8);  // one ring per consumer group
+  static constexpr int STAGES_FIT = SMEM_BUDGET / ((A_ST + B_ST) * 8);
   static constexpr int STAGES = STAGES_FIT < MAX_STAGES ? STAGES_FIT : MAX_STAGES;
   static constexpr int BYTES = STAGES * SLOT * 8;
   static_assert(STAGES >= 3, "ring too shallow");
-  // (two-group rings never stage C: that instantiation reads C from global)
-  static_assert(GRP_ == 2 || (CS < STAGES && BN % CPS == 0 && CPS * CP <= SLOT), "C staging must leave a slab slot");
+  static_assert(CS < STAGES && BN % CPS == 0 && CPS * CP <= SLOT, "C staging must leave a slab slot");
 };
 constexpr int GROUP_M = MYD_FAST_GROUP_M;
 constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is probed
@@ -183,7 +182,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, int GRP>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -191,13 +190,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   using namespace fast;
   constexpr int SPLIT_M = TILE_M / BM, SPLIT_N = TILE_N / BN;
   constexpr int SPLIT = SPLIT_M * SPLIT_N;  // work units per full tile
-  // GRP consumer groups (1, or 2: two independent pipelines per CTA -- each
-  // with half the consumer and producer warps, its own ring and barriers and
-  // its own unit sequence, the second half a unit behind -- so one group's
-  // unit boundary (C write-back and reload) overlaps the other's K loop).
-  static_assert(GRP == 1 || (GRP == 2 && !SKM), "consumer groups");
-  constexpr int CWARPS = CONSUMER_WARPS / GRP, PWARPS = PRODUCER_WARPS / GRP;
-  using R = Ring<BM, BN, BKT, GRP>;
+  using R = Ring<BM, BN, BKT>;
   constexpr int BK = R::BK;          // K slab per stage
   constexpr int KSTEPS = BK / 4;     // DMMA k-steps per slab
   constexpr int AP = R::AP, BP = R::BP;
@@ -205,11 +198,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   constexpr int SLOT = R::SLOT, A_STAGE = R::A_ST;
   constexpr int CP = R::CP, CPS = R::CPS, CS = R::CS;
   constexpr int WARPS_N = BN / WN;
-  constexpr int WARPS_M = CWARPS / WARPS_N;
+  constexpr int WARPS_M = CONSUMER_WARPS / WARPS_N;
   constexpr int WM = BM / WARPS_M;
   constexpr int FM = WM / 8, FN = WN / 8;
-  constexpr int RW = BN / PWARPS;  // B rows staged by each producer warp
-  static_assert(WARPS_M * WARPS_N == CWARPS && FM >= 1 && RW >= 8, "tile shape");
+  constexpr int RW = BN / PRODUCER_WARPS;  // B rows staged by each producer warp
+  static_assert(WARPS_M * WARPS_N == CONSUMER_WARPS && FM >= 1 && RW >= 8, "tile shape");
   // Full tiles of the unit-mode kernel read their C block straight from
   // global memory (the producers prefetch it to L2 when they start the
   // unit; the consumers read it into each fragment pair right after storing
@@ -220,26 +213,18 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (profiles/c_from_global_r01.log); the stream-K kernel's full tiles too
   // (2048^3, all stream-K, +0.6 %).  Narrower units keep the ring path
   // (measured slower this way).
-  constexpr bool CG = CGT && MYD_CGLOBAL && VEC == 2 && BM == 128 && (BN == 128 || GRP == 2) && (!SKM || MYD_CGLOBAL_SK);
+  constexpr bool CG = CGT && MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
   // The full-tile instantiation launched for an unaligned C (odd ldc, see
   // launch_one): its C columns alternate 16-byte alignment, so every other
   // column is still staged by bulk copy and stored with 16-byte stores.  Kept
   // out of the other instantiations, whose code this slows (2-5 %).
   constexpr bool ODD_C = VEC == 2 && BM == 128 && BN == 128 && !CGT;
 
-  extern __shared__ __align__(128) double smem_all[];  // per group: STAGES slots of [A slab | B slab]
-  __shared__ __align__(8) uint64_t full_bar_all[MAX_STAGES * GRP];
-  __shared__ __align__(8) uint64_t empty_bar_all[MAX_STAGES * GRP];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int grp = GRP == 1 ? 0 : (warp < CONSUMER_WARPS ? warp / CWARPS : (warp - CONSUMER_WARPS) / PWARPS);
-  double *const smem = smem_all + grp * (STAGES * SLOT);
-  uint64_t *const full_bar = full_bar_all + grp * MAX_STAGES;
-  uint64_t *const empty_bar = empty_bar_all + grp * MAX_STAGES;
-  // the group's place in the persistent round-robin: virtual CTA vb of vg
-  const int vb = (int)blockIdx.x * GRP + grp, vg = (int)gridDim.x * GRP;
+  extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
+  __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
+  __shared__ __align__(8) uint64_t empty_bar[MAX_STAGES];
 
-  // Work unit u (persistent CTA / group vb takes u = vb, vb + vg, ...): full
+  // Work unit u (persistent CTA b takes u = b, b + gridDim.x, ...): full
   // 128x128 tile tile0 + u / SPLIT in the grouped raster (GROUP_M tile-rows
   // per band, column-major inside a band), sub-block u % SPLIT of it.  With
   // edge = ns > 0 the ragged last tile column is kept out of the raster and
@@ -273,7 +258,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   const bool ragged = (M % TILE_M) != 0 || (N % TILE_N) != 0;  // else no unit can be empty
   auto next_unit = [&](int u) {
     if (!ragged) return u;
-    for (; u < units; u += vg) {
+    for (; u < units; u += gridDim.x) {
       int m0, n0;
       unit_origin(u, m0, n0);
       if (m0 < M && n0 < N) break;
@@ -281,6 +266,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     return u;
   };
 
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
 #ifdef MYD_TIMELINE
   int unit_ord = 0;  // units finished by this consumer warp (timeline marks)
   if (tid == 0 && !after_main) atomicMin(&g_tl[0], gtimer());
@@ -308,31 +295,17 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   };
   constexpr int SK0 = 1 << 30;  // stream-K cursors (the planner keeps iterations < 2^30)
   const int sk_iters = (int)sk.iters, sk_dp = (int)sk.dp_tiles;
-  const int sk_per = sk_iters / vg, sk_rem = sk_iters % vg;
-  const int sk_lo = sk_per * vb + min(vb, sk_rem);
-  const int sk_hi = sk_lo + sk_per + (vb < sk_rem ? 1 : 0);
-  // Group 1 of a two-group CTA starts half a unit behind group 0: its first
-  // unit u0 runs only its lower K slabs first (C to C: the exact accumulator
-  // goes through C, like k-chunking), and the upper slabs last, from C (the
-  // DEF cursor) -- the same chain per element, so C is bitwise unchanged.
-  constexpr int DEF = 1 << 29;  // cursor of the deferred upper half (planner keeps units < 2^29)
-  const int u_first = SKM ? 0 : next_unit(vb);
-  const bool defer = GRP == 2 && grp == 1 && KT >= 2 && u_first < units;
+  const int sk_per = sk_iters / (int)gridDim.x, sk_rem = sk_iters % (int)gridDim.x;
+  const int sk_lo = sk_per * (int)blockIdx.x + min((int)blockIdx.x, sk_rem);
+  const int sk_hi = sk_lo + sk_per + ((int)blockIdx.x < sk_rem ? 1 : 0);
   auto seg_at = [&](int cur, Seg &sg) -> bool {
     if constexpr (!SKM) {
-      sg.from_c = sg.to_c = true;
-      sg.slot = -1;
-      if (cur >= DEF) {
-        if (!defer || cur != DEF + u_first) return false;
-        unit_origin(u_first, sg.m0, sg.n0);
-        sg.kb = KT / 2;
-        sg.ke = KT;
-        return true;
-      }
       if (cur >= units) return false;
       unit_origin(cur, sg.m0, sg.n0);
       sg.kb = 0;
-      sg.ke = (defer && cur == u_first) ? KT / 2 : KT;
+      sg.ke = KT;
+      sg.from_c = sg.to_c = true;
+      sg.slot = -1;
       return true;
     } else {
       if (cur < SK0) {  // data-parallel tile
@@ -352,24 +325,22 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       sg.ke = KT - l0;
       sg.from_c = sg.kb == 0;
       sg.to_c = sg.ke == KT;
-      sg.slot = sg.to_c ? vb : vb - 1;  // upper part reads b; lower part writes b - 1
+      sg.slot = sg.to_c ? (int)blockIdx.x : (int)blockIdx.x - 1;  // upper part reads b; lower part writes b - 1
       return true;
     }
   };
   auto seg_first = [&]() -> int {
     if constexpr (!SKM) {
-      return u_first;
+      return next_unit(blockIdx.x);
     } else {
-      return vb < sk_dp ? vb : SK0 + sk_lo;
+      return (int)blockIdx.x < sk_dp ? (int)blockIdx.x : SK0 + sk_lo;
     }
   };
   auto seg_next = [&](int cur, const Seg &sg) -> int {
     if constexpr (!SKM) {
-      if (cur >= DEF) return 0x7fffffff;
-      const int nx = next_unit(cur + vg);
-      return (nx >= units && defer) ? DEF + u_first : nx;
+      return next_unit(cur + gridDim.x);
     } else {
-      if (cur < SK0) return cur + vg < sk_dp ? cur + vg : SK0 + sk_lo;
+      if (cur < SK0) return cur + (int)gridDim.x < sk_dp ? cur + (int)gridDim.x : SK0 + sk_lo;
       const int it = cur - SK0;
       return SK0 + (it / KT) * KT + (KT - sg.kb);
     }
@@ -378,9 +349,9 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 
   if (tid == 0) {
 #pragma unroll
-    for (int s = 0; s < STAGES * GRP; ++s) {  // (group g's barriers at g * MAX_STAGES)
-      mbar_init(&full_bar_all[(s / STAGES) * MAX_STAGES + s % STAGES], PWARPS);   // one arrival per producer warp
-      mbar_init(&empty_bar_all[(s / STAGES) * MAX_STAGES + s % STAGES], CWARPS);  // one arrival per consumer warp
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], PRODUCER_WARPS);   // one arrival per producer warp
+      mbar_init(&empty_bar[s], CONSUMER_WARPS);  // one arrival per consumer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -402,7 +373,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   if (warp >= CONSUMER_WARPS) {
     // ================= producers: pack_a / pack_b equivalent =================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-    const int pw = (warp - CONSUMER_WARPS) % PWARPS;  // producer warp within the group
+    const int pw = warp - CONSUMER_WARPS;
     const bool c_aligned = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
     const bool c16 = ODD_C && ((uintptr_t)C % 16 == 0);
 #ifdef MYD_TIMELINE
@@ -439,8 +410,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // critical path and spread in time instead of bursting at unit start.
       if (CG && (!ep.blas || ep.beta != 0.0) && sg.from_c) {  // BLAS: C is read by the epilogue
         const int rows = max(0, min(BM, M - m0));
-        const int col = pw * (BN / PWARPS) + lane;
-        if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PWARPS && n0 + col < N)
+        const int col = pw * (BN / PRODUCER_WARPS) + lane;
+        if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PRODUCER_WARPS && n0 + col < N)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(C + (int64_t)(n0 + col) * ldc + m0),
                        "r"(rows * 8)
                        : "memory");
@@ -456,7 +427,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           // Whole aligned columns go by bulk copy; otherwise only the valid
           // rows of valid columns are copied (8-byte cp.async); rows/columns
           // outside C stay stale -- their accumulators are never stored.
-          constexpr int CW = CPS / PWARPS;
+          constexpr int CW = CPS / PRODUCER_WARPS;
           const int rows = max(0, min(BM, M - m0));  // 0 for a unit wholly below C
           // a column goes by bulk copy when its first valid element is 16-byte
           // aligned and it holds an even number of rows (with an odd ldc,
@@ -512,7 +483,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         double *as = smem + slot * SLOT;
         double *bs = as + A_STAGE;
         if (interior && kbase + BK <= K) {
-          constexpr int A_ROWS = BK / PWARPS;  // k-rows of A per producer warp
+          constexpr int A_ROWS = BK / PRODUCER_WARPS;  // k-rows of A per producer warp
           constexpr uint32_t BYTES = (A_ROWS * BM + RW * BK) * 8;
           if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], BYTES);
           __syncwarp();
@@ -545,8 +516,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
         // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
         // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
 #pragma unroll
-        for (int i = 0; i < BK * BM / (VEC * 32 * PWARPS); ++i) {
-          const int e = ((pw * 32 + lane) + i * 32 * PWARPS) * VEC;
+        for (int i = 0; i < BK * BM / (VEC * 32 * PRODUCER_WARPS); ++i) {
+          const int e = ((pw * 32 + lane) + i * 32 * PRODUCER_WARPS) * VEC;
           const int kk = e / BM, mm = e % BM;
           const int gk = kbase + kk, gmr = m0 + mm;
           int bytes = 0;
@@ -594,8 +565,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
   if (!after_main) asm volatile("griddepcontrol.wait;\n" "griddepcontrol.launch_dependents;\n" ::: "memory");
   // ================= consumers: loops 2/1 + micro-kernel =================
-  const int cw = warp % CWARPS;  // consumer warp within the group
-  const int wm = cw % WARPS_M, wn = cw / WARPS_M;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int r = lane >> 2, q = lane & 3;
   const int a_off = q * AP + wm * WM + r;    // + kk*4*AP + i*8
   const int b_off = (wn * WN + r) * BP + q;  // + j*8*BP + kk*4
@@ -661,7 +631,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (s, w) carries the launch's epoch once they are written.
   constexpr int NV2 = FM * FN;  // double2 per lane
   auto part_base = [&](int slot) -> double2 * {
-    return reinterpret_cast<double2 *>(sk.work) + ((int64_t)slot * CONSUMER_WARPS + cw) * NV2 * 32 + lane;
+    return reinterpret_cast<double2 *>(sk.work) + ((int64_t)slot * CONSUMER_WARPS + warp) * NV2 * 32 + lane;
   };
   auto store_partial = [&](int slot) {
     double2 *p = part_base(slot);
@@ -672,12 +642,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     __threadfence();
     __syncwarp();
     if (lane == 0)
-      asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(sk.flags + slot * CONSUMER_WARPS + cw),
+      asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(sk.flags + slot * CONSUMER_WARPS + warp),
                    "l"(sk.epoch)
                    : "memory");
   };
   auto load_partial = [&](int slot) {
-    const unsigned long long *f = sk.flags + slot * CONSUMER_WARPS + cw;
+    const unsigned long long *f = sk.flags + slot * CONSUMER_WARPS + warp;
     for (;;) {
       unsigned long long v;
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(f) : "memory");
@@ -718,7 +688,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     }
     if constexpr (CG) {
       if (!ep.blas) {
-        if (GRP == 2 && sg.kb > 0) __syncwarp();  // deferred half: C written by other lanes of this warp
         const bool inside = c_inside(sg);
 #pragma unroll
         for (int i = 0; i < FM; ++i)
@@ -851,9 +820,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           // each fragment pair right after that pair is stored, so the
           // shared-memory reads overlap the global write-back.
           const uint32_t gn = g + NS;
-          // (the BLAS epilogue starts from 0; a deferred half of this same
-          // unit reads C only after all of it is stored, in init_acc)
-          const bool pre = has_next && nsg.from_c && !ep.blas && !(nsg.m0 == sg.m0 && nsg.n0 == sg.n0);
+          const bool pre = has_next && nsg.from_c && !ep.blas;  // the BLAS epilogue starts from 0
           const bool n_inside = CG && pre && c_inside(nsg);
           const int nrow0 = nsg.m0 + wm * WM + 2 * q, ncol0 = nsg.n0 + wn * WN + r;
           if (!CG && pre)
@@ -945,7 +912,7 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, int GRP = 1>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -957,25 +924,25 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, GRP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<BM, BN, BK, GRP>::BYTES * GRP);
+    cudaError_t e =
+        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
   }
   // persistent: at most one CTA per SM, each walking units b, b+grid, ...
-  // (GRP groups per CTA: virtual CTAs GRP*b + g over the units)
-  const unsigned grid = std::min<unsigned>((units + GRP - 1) / GRP, (unsigned)sm_count());
+  const unsigned grid = std::min<unsigned>(units, (unsigned)sm_count());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = Ring<BM, BN, BK, GRP>::BYTES * GRP;
+  cfg.dynamicSmemBytes = Ring<BM, BN, BK>::BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, GRP>, M, N, K, A, lda, B, ldb, C, ldc,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, M, N, K, A, lda, B, ldb, C, ldc,
                                      tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
@@ -1009,21 +976,6 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   if (rk) MYD_LAUNCH(false, true);
   MYD_LAUNCH(false, false);
 #undef MYD_LAUNCH
-}
-
-// Two consumer groups per CTA over 128x64 units (C from global, so an aligned
-// C and the my_dgemm contract: the deferred half goes through C).
-template <int BK>
-cudaError_t launch_two_group(unsigned units, int M, int N, int K, const double *A, int64_t lda, const double *B,
-                             int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
-                             int after_main, cudaStream_t st) {
-  const bool rk = MYD_SKIP_ZERO_KSTEPS && K % BK != 0 && BK - K % BK >= 4;
-  const Epilogue ep{};
-  if (rk)
-    return launch_kernel<2, 128, 64, BK, false, true, true, 2>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
-                                                               tiles_n, tile0, edge, after_main, st, StreamK{});
-  return launch_kernel<2, 128, 64, BK, false, true, false, 2>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m,
-                                                              tiles_n, tile0, edge, after_main, st, StreamK{});
 }
 
 template <int VEC>
@@ -1346,12 +1298,6 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
             M, N, K, (long long)tiles_m, tiles_n, small_v ? "small" : (streamk ? "stream-K" : "units"), split, sk_split, q,
             raster_m, raster_n, edge, small_v);
   if (small_v > 0) return launch_dgemm_small(small_v, M, N, K, A, lda, B, ldb, C, ldc, stream, ep, vec2);
-  if (force_split == 3) {  // two consumer groups per CTA over 128x64 units (else one group, below)
-    const bool c_al = (ldc % 2 == 0) && ((uintptr_t)C % 16 == 0);
-    if (vec2 && c_al && !ep.blas)
-      return launch_two_group<16>((unsigned)(tiles * 2), M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
-                                  stream);
-  }
   if (streamk) {
     SkWorkspace ws;
     cudaError_t e = ws.alloc((int)G, stream);
@@ -1426,7 +1372,6 @@ bool plan_geometry(int plan, int K, bool vec2, int &bm, int &bn, int &bk, int &s
       }
       return true;
     case 2: bm = 128, bn = 64, bk = Ring<128, 64>::BK, stages = Ring<128, 64>::STAGES; return true;
-    case 3: bm = 128, bn = 64, bk = 16, stages = Ring<128, 64, 16, 2>::STAGES; return true;  // per group
     case 4: bm = 128, bn = 32, bk = Ring<128, 32>::BK, stages = Ring<128, 32>::STAGES; return true;
     case 8: bm = 64, bn = 32, bk = Ring<64, 32>::BK, stages = Ring<64, 32>::STAGES; return true;
     case 16:

@@ -77,7 +77,7 @@ extern "C" int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, int
     // small-block kernel variants (plans 65..74) for problems up to a few
     // waves of tiles; larger problems skip them (each would take minutes)
     const long long tiles = (long long)((m + 127) / 128) * ((n + 127) / 128);
-    const int plans[] = {0, 1, 2, 3, 4, 8, 16, 32, 34, 36, 40, 65, 66, 67, 68, 69, 70, 71, 72, 73, 74};
+    const int plans[] = {0, 1, 2, 4, 8, 16, 32, 34, 36, 40, 65, 66, 67, 68, 69, 70, 71, 72, 73, 74};
     for (int plan : plans) {
       if (plan >= 64 && tiles > 4 * 148) continue;
       const Epilogue ep{};

@@ -37,7 +37,7 @@ from . import _capi
 from . import engine
 
 AXES = ("bm", "bn", "bk", "stages")
-PLANS = (1, 2, 3, 4, 8, 16, 32, 34, 36, 40) + tuple(range(65, 75))
+PLANS = (1, 2, 4, 8, 16, 32, 34, 36, 40) + tuple(range(65, 75))
 REF_SEED = 42  # the reference's default Config.seed (config.py)
 
 

@@ -1,4 +1,4 @@
-"""Two consumer groups per CTA (plan 3: 128x64 units, each group its own ring
+"""Two consumer groups per CTA (plan 3, an experiment removed after this probe; see git history) against the heuristic, full
 and unit sequence, the second half a unit behind) against the heuristic, full
 tiles and one-group 128x64 units: device time of back-to-back calls and a
 bitwise check against the heuristic's C (development aid,
