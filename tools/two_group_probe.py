@@ -1,8 +1,8 @@
-"""Two consumer groups per CTA (plan 3, an experiment removed after this probe; see git history) against the heuristic, full
-and unit sequence, the second half a unit behind) against the heuristic, full
-tiles and one-group 128x64 units: device time of back-to-back calls and a
-bitwise check against the heuristic's C (development aid,
-profiles/r02/two_group_r02*.log).
+"""Two consumer groups per CTA (plan 3 -- an experiment removed after this
+probe, see git history: 128x64 units, each group its own ring and unit
+sequence, the second half a unit behind) against the heuristic, full tiles
+and one-group 128x64 units: device time of back-to-back calls and a bitwise
+check against the heuristic's C (profiles/r02/two_group_r02a.log).
 
   python tools/two_group_probe.py [MxNxK ...]
 """
