@@ -102,6 +102,9 @@ __device__ unsigned long long g_fast_prof[8];
 #define MYD_L2_HINTS 0  // 1: A slabs evict_last, B slabs evict_first (full tiles); 2: the reverse;
                         // 3: A evict_last only; 4: B evict_first only (profiles/r02/l2_hints_r02*.log)
 #endif
+#ifndef MYD_L2_PERSIST_MB
+#define MYD_L2_PERSIST_MB 0  // > 0 (with MYD_L2_HINTS): persisting-L2 carve-out for evict_last lines, MB
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -924,6 +927,10 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   cudaGetDevice(&dev);
   const uint64_t bit = 1ull << (dev & 63);
   if (!(attr_done.load(std::memory_order_acquire) & bit)) {
+    if constexpr (MYD_L2_PERSIST_MB > 0) {  // experiment builds: bound the evict_last (persisting) lines
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)MYD_L2_PERSIST_MB << 20);
+      cudaGetLastError();
+    }
     cudaError_t e =
         cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Ring<BM, BN, BK>::BYTES);
