@@ -93,16 +93,43 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   const double flops = 2.0 * m * (double)n * k;
   // (the column panels and k-chunks are bitwise the one call only on the tiled path)
   const bool pipelined = flops > 4e9 && n >= 1024 && path_kind(m, n, flags) == MY_DGEMM_PATH_TILED;
-  int64_t nc0 = n, panel = n;
+  // Column group 0 is computed in k-chunks while A uploads; it only needs to
+  // be wide enough that each chunk's GEMM outlasts the next chunk's upload
+  // (flop per uploaded byte 2 m nc0 / (8 (m + nc0)) against 36.7 TF over
+  // 55 GB/s, with 25 % margin), and no wider: its C block is the upload the
+  // first GEMM waits for.  Small m cannot hide A at all; then half of C.
+  // The remaining columns go in panels of ~n/8 whose last one is cut into
+  // halves down to 512 columns, so the download after the final GEMM is short.
+  int64_t nc0 = n;
+  std::vector<int64_t> pj0, pnc;  // panels after group 0: first column, width
   if (pipelined) {
+    const double need = 1.25 * 8.0 * 36.7e12 / (2.0 * 55e9);  // m nc0 / (m + nc0) >= need
     nc0 = std::max<int64_t>(128, (n / 2) / 128 * 128);
-    panel = std::max<int64_t>(512, ((n / 8 + 127) / 128) * 128);
+    if ((double)m > need * 1.05) {
+      const double w = need * m / (m - need);
+      nc0 = std::min<int64_t>(nc0, std::max<int64_t>(1024, ((int64_t)w + 127) / 128 * 128));
+    }
+    const int64_t panel = std::max<int64_t>(512, ((n / 8 + 127) / 128) * 128);
+    for (int64_t j = nc0; j < n;) {
+      int64_t wdt = std::min<int64_t>(panel, n - j);
+      pj0.push_back(j);
+      pnc.push_back(wdt);
+      j += wdt;
+    }
+    while (!pnc.empty() && pnc.back() >= 1024) {  // halve the last panel: 4096 -> 2048, 1024, 512, 512
+      const int64_t last = pnc.back(), h = (last / 2 + 127) / 128 * 128;
+      if (last - h < 512) break;
+      pnc.back() = h;
+      pj0.push_back(pj0.back() + h);
+      pnc.push_back(last - h);
+      if (last - h < 1024) break;
+    }
   }
-  const size_t panels = 1 + (size_t)((n - nc0 + panel - 1) / panel);  // group 0 + whole panels
-  auto panel_j0 = [&](size_t p) -> int64_t { return p == 0 ? 0 : nc0 + (int64_t)(p - 1) * panel; };
-  auto panel_nc = [&](size_t p) -> int64_t { return p == 0 ? nc0 : std::min<int64_t>(panel, n - panel_j0(p)); };
-  int64_t kchunk = k;
-  if (pipelined && k >= 256) kchunk = (((k + 7) / 8) + 15) / 16 * 16;
+  const size_t panels = 1 + pj0.size();  // group 0 + whole panels
+  auto panel_j0 = [&](size_t p) -> int64_t { return p == 0 ? 0 : pj0[p - 1]; };
+  auto panel_nc = [&](size_t p) -> int64_t { return p == 0 ? nc0 : pnc[p - 1]; };
+  int64_t kchunk = k;  // multiples of 16: bitwise the unchunked GEMM
+  if (pipelined && k >= 256) kchunk = std::min<int64_t>(1024, (((k + 7) / 8) + 15) / 16 * 16);
   const size_t kchunks = (size_t)((k + kchunk - 1) / kchunk);
   if ((e = ensure_streams(w, std::max(panels, kchunks) + 1)) != cudaSuccess)
     return capi_cuda_fail(e, "stream setup");
