@@ -35,13 +35,6 @@
 
 namespace myd {
 
-#ifndef MYD_SMALL_PD
-#define MYD_SMALL_PD 4  // fragment register buffers of the full-slab loop (k-steps prefetched + 1)
-#endif
-#ifndef MYD_SMALL_PD_MAXF
-#define MYD_SMALL_PD_MAXF 4  // ... for warps with at most this many fragments (FM + FN); 2 buffers above
-#endif
-
 namespace small {
 constexpr int WARPS = 4;  // one per SM sub-partition when a CTA has the SM alone
 constexpr int THREADS = WARPS * 32;
@@ -162,32 +155,6 @@ __global__ void __launch_bounds__(small::THREADS)
       for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fb[j], fa[i]);
   };
 
-  // Full slabs: fragments prefetched PD - 1 k-steps ahead through PD register
-  // buffers (compile-time indices after unrolling), so a k-step's DMMA does
-  // not wait on its own shared-memory loads -- with one or two warps per
-  // sub-partition the K chain is latency-bound (profiles/r02/small_kernel_r02*.log).
-  constexpr int PD = (FM + FN <= MYD_SMALL_PD_MAXF) ? MYD_SMALL_PD : 2;
-  auto slab_full = [&](const double *as, const double *bs) {
-    double fa[PD][FM], fb[PD][FN];
-    auto load = [&](int buf, int kk) {
-#pragma unroll
-      for (int i = 0; i < FM; ++i) fa[buf][i] = as[a_off + kk * 4 * AP + i * 8];
-#pragma unroll
-      for (int j = 0; j < FN; ++j) fb[buf][j] = bs[b_off + kk * 4 + j * 8 * BP];
-    };
-#pragma unroll
-    for (int p = 0; p < PD - 1; ++p)
-      if (p < KSTEPS) load(p, p);
-#pragma unroll
-    for (int kk = 0; kk < KSTEPS; ++kk) {
-      if (kk + PD - 1 < KSTEPS) load((kk + PD - 1) % PD, kk + PD - 1);
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma_884(acc[i][j][0], acc[i][j][1], fb[kk % PD][j], fa[kk % PD][i]);
-    }
-  };
-
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();  // slab kt landed for every thread; slot (kt - 1) % STAGES free
@@ -199,7 +166,8 @@ __global__ void __launch_bounds__(small::THREADS)
     const double *as = smem + (kt % STAGES) * SLOT;
     const double *bs = as + A_ST;
     if (kt + 1 < KT || K % BK == 0) {
-      slab_full(as, bs);
+#pragma unroll
+      for (int kk = 0; kk < KSTEPS; ++kk) kstep(as, bs, kk);
     } else {
       // last slab of a ragged K: only the k-groups holding some k < K
       const int nsteps = (K - kt * BK + 3) / 4;
