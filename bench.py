@@ -614,8 +614,9 @@ def measure_e2e(args, m, nloc, k, seeds, j0, rank, world, n_total, plan, A, B, C
 
 def load_traffic(workload, world=1):
     """dram bytes per call of dgemm_fast_kernel from the committed ncu --set
-    full summary (profiles/traffic.json) when it was captured on this
-    workload at one GPU (the per-rank call differs at N > 1), else None."""
+    full summary (profiles/traffic.json, one entry per workload) when it was
+    captured on this workload at one GPU (the per-rank call differs at
+    N > 1), else None."""
     p = os.path.join(REPO, "profiles", "traffic.json")
     try:
         with open(p) as f:
@@ -624,7 +625,10 @@ def load_traffic(workload, world=1):
         return None
     if world != 1:
         return None
-    return t.get("dram_bytes_per_launch") if str(t.get("workload", "")).startswith(workload + " ") else None
+    entry = t.get("workloads", {}).get(workload) if "workloads" in t else t
+    if not entry or not str(entry.get("workload", "")).startswith(workload + " "):
+        return None
+    return entry.get("dram_bytes_per_launch")
 
 
 def under_launcher() -> bool:
