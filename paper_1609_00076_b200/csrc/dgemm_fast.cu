@@ -1288,7 +1288,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         if (c < sbest) sbest = c, small_v = v;
       }
     }
-  } else if (force_split == 0 && tiles <= 2 * G) {
+  } else if (force_split == 0 && tiles <= 2 * G && g_max_ctas.load(std::memory_order_relaxed) == 0) {
+    // (not under an SM cap: its grid is the block count, not a persistent
+    // grid the cap could bound; results do not depend on the choice)
     double sbest = plan_best;
     for (int v = 1; v <= small_variants(); ++v) {
       const double c = small_cost_us(v, M, N, K, (int)G);

@@ -797,11 +797,12 @@ def test_back_to_back_dependent_calls_stream_ordered(torch_cuda, shape):
         assert torch_cuda.equal(got[0], want[0]) and torch_cuda.equal(got[1], want[1])
 
 
-@pytest.mark.parametrize("shape", [(4093, 4099, 300), (2048, 2048, 512), (700, 900, 1000)])
+@pytest.mark.parametrize("shape", [(4093, 4099, 300), (2048, 2048, 512), (700, 900, 1000), (256, 256, 256)])
 def test_sm_cap_changes_speed_never_results(torch_cuda, shape):
     """my_dgemm_set_max_ctas: the persistent grid on 100, 37 or 1 SMs gives
     bitwise the all-SM result (different plans and unit assignment, same
-    per-element arithmetic)."""
+    per-element arithmetic); 256^3 runs on the small-block kernel without a
+    cap and on the persistent grid under one."""
     m, n, k = shape
     a, b, c, _ = dev_operands(torch_cuda, m, n, k)
     want = c.clone()
