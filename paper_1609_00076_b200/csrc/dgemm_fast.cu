@@ -105,9 +105,6 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_L2_PERSIST_MB
 #define MYD_L2_PERSIST_MB 0  // > 0 (with MYD_L2_HINTS): persisting-L2 carve-out for evict_last lines, MB
 #endif
-#ifndef MYD_OC
-#define MYD_OC 1  // full tiles with an unaligned C: C from global with realigned pairs (0: ring-staged, 8-byte halves)
-#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -188,7 +185,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, int CGT, bool RK>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -219,20 +216,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // (profiles/c_from_global_r01.log); the stream-K kernel's full tiles too
   // (2048^3, all stream-K, +0.6 %).  Narrower units keep the ring path
   // (measured slower this way).
-  constexpr bool CG = CGT != 0 && MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
-  // CGT == 2: C from global with an unaligned C (odd ldc or an 8-byte aligned
-  // base).  A lane's fragment pair (rows 2q, 2q+1 of one column) then
-  // straddles a 16-byte boundary in every other column; those columns load
-  // and store the aligned pairs (2q+1, 2q+2) instead and pass the odd row on
-  // to the neighbouring lane with one quad shuffle per fragment (the
-  // column's first and last rows go alone), so every interior access stays
-  // 16 bytes wide.
-  constexpr bool OC = CG && CGT == 2;
+  constexpr bool CG = CGT && MYD_CGLOBAL && VEC == 2 && BM == 128 && BN == 128 && (!SKM || MYD_CGLOBAL_SK);
   // The full-tile instantiation launched for an unaligned C (odd ldc, see
   // launch_one): its C columns alternate 16-byte alignment, so every other
   // column is still staged by bulk copy and stored with 16-byte stores.  Kept
   // out of the other instantiations, whose code this slows (2-5 %).
-  constexpr bool ODD_C = VEC == 2 && BM == 128 && BN == 128 && CGT == 0;
+  constexpr bool ODD_C = VEC == 2 && BM == 128 && BN == 128 && !CGT;
 
   extern __shared__ __align__(128) double smem[];  // STAGES slots of [A slab | B slab]
   __shared__ __align__(8) uint64_t full_bar[MAX_STAGES];
@@ -425,15 +414,10 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       if (CG && (!ep.blas || ep.beta != 0.0) && sg.from_c) {  // BLAS: C is read by the epilogue
         const int rows = max(0, min(BM, M - m0));
         const int col = pw * (BN / PRODUCER_WARPS) + lane;
-        if (lane < BN / PRODUCER_WARPS && n0 + col < N && rows > 0) {
-          // the 16-byte aligned part of the column's valid rows (OC: skip a
-          // misaligned first element; never past the valid region)
-          const double *cp = C + (int64_t)(n0 + col) * ldc + m0;
-          const int skip = ((uintptr_t)cp & 15) ? 1 : 0;
-          const int n16 = ((rows - skip) / 2) * 16;
-          if ((c_aligned || OC) && n16 > 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(cp + skip), "r"(n16) : "memory");
-        }
+        if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PRODUCER_WARPS && n0 + col < N)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(C + (int64_t)(n0 + col) * ldc + m0),
+                       "r"(rows * 8)
+                       : "memory");
       }
       if (!CG && !ep.blas && sg.from_c) {
         const bool c_bulk = c_aligned && (m0 + BM <= M) && (n0 + BN <= N);
@@ -696,59 +680,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       acc[i][j][1] = (row + 1 < M && col < N) ? __ldcg(cp + 1) : 0.0;
     }
   };
-  auto c_inside = [&](const Seg &s) { return (c_aligned || OC) && s.m0 + BM <= M && s.n0 + BN <= N; };
-  // OC: does this lane's column start at an odd element (8 bytes past a
-  // 16-byte boundary)?  Columns n0 + wn*WN + r + 8j: the parity only
-  // depends on r (and on the base), so it is lane-constant.
-  const bool oc_shift = OC && ((((int64_t)r * ldc) + (((uintptr_t)C & 15) ? 1 : 0)) & 1);
-  const int oc_rot_dn = (lane & ~3) | ((q + 3) & 3), oc_rot_up = (lane & ~3) | ((q + 1) & 3);
-  // OC interior unit: C block -> accumulators, realigned pairs (see OC)
-  auto load_c_oc = [&](int row0, int col0) {
-#pragma unroll
-    for (int j = 0; j < FN; ++j) {
-      double s_prev = 0.0;
-#pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        const double *cp = C + (int64_t)(col0 + j * 8) * ldc + row0 + i * 8;
-        double2 v;
-        if (oc_shift && i == FM - 1 && q == 3) {  // the column's last row goes alone
-          v.x = __ldcg(cp + 1);
-          v.y = 0.0;
-        } else {
-          v = __ldcg(reinterpret_cast<const double2 *>(cp + (oc_shift ? 1 : 0)));
-        }
-        const double sh = __shfl_sync(0xffffffffu, v.y, oc_rot_dn);  // lane q-1's (or q=3's, one fragment up)
-        if (oc_shift) {
-          acc[i][j][1] = v.x;
-          acc[i][j][0] = q ? sh : (i == 0 ? __ldcg(cp) : s_prev);  // the column's first row goes alone
-        } else {
-          acc[i][j][0] = v.x;
-          acc[i][j][1] = v.y;
-        }
-        s_prev = sh;
-      }
-    }
-  };
-  // OC interior unit: accumulators -> C, realigned pairs
-  auto store_c_oc = [&](int row0, int col0) {
-#pragma unroll
-    for (int j = 0; j < FN; ++j) {
-#pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        double *cp = C + (int64_t)(col0 + j * 8) * ldc + row0 + i * 8;
-        const double nx = __shfl_sync(0xffffffffu, acc[i][j][0], oc_rot_up);  // lane q+1's row (q=3: next fragment's)
-        if (!oc_shift) {
-          *reinterpret_cast<double2 *>(cp) = make_double2(acc[i][j][0], acc[i][j][1]);
-        } else if (q < 3) {
-          *reinterpret_cast<double2 *>(cp + 1) = make_double2(acc[i][j][1], nx);
-          if (i == 0 && q == 0) cp[0] = acc[0][j][0];
-        } else if (i > 0) {  // q = 3: rows 8(i-1)+7 and 8i of the warp tile (cp is row 8i + 6)
-          *reinterpret_cast<double2 *>(cp - 7) = make_double2(acc[i - 1][j][1], nx);
-        }
-      }
-      if (oc_shift && q == 3) C[(int64_t)(col0 + j * 8) * ldc + row0 + (FM - 1) * 8 + 1] = acc[FM - 1][j][1];
-    }
-  };
+  auto c_inside = [&](const Seg &s) { return c_aligned && s.m0 + BM <= M && s.n0 + BN <= N; };
   constexpr int CSR = CG ? 0 : CS;  // ring slots a unit's C block occupies
   // accumulator initialisation of a segment whose C block (if any) sits at
   // ring position gpos; returns the ring position of its first slab
@@ -760,12 +692,6 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     if constexpr (CG) {
       if (!ep.blas) {
         const bool inside = c_inside(sg);
-        if constexpr (OC) {
-          if (inside) {
-            load_c_oc(sg.m0 + wm * WM + 2 * q, sg.n0 + wn * WN + r);
-            return gpos;
-          }
-        }
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -884,18 +810,12 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
             if (row + 1 < M) v1 = fma(ep.alpha, v1, ep.beta * cp[1]);
           }
       }
-      if constexpr (OC) {
-        if (!ep.blas && sg.m0 + BM <= M && sg.n0 + BN <= N) {
-          store_c_oc(row0, col0);
-          stored = true;
-        }
-      }
 #if MYD_EP_SHFL
       // Interior units: lanes r < 4 and r >= 4 (lane ^ 16) swap one pair of
       // every two row-fragments so each warp store writes 4 columns x 128
       // contiguous bytes instead of 8 columns x 64: half the cache lines per
       // store instruction, which is what bounds the write-back of a unit.
-      if constexpr (FM % 2 == 0 && !OC) {
+      if constexpr (FM % 2 == 0) {
         if (c_aligned && sg.m0 + BM <= M && sg.n0 + BN <= N) {
           const bool lo = r < 4;
           const int rowb = row0 + (lo ? 0 : 8), colb = col0 - (lo ? 0 : 4);
@@ -995,7 +915,7 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, int CGT, bool RK>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -1056,18 +976,12 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
                                                         tile0, edge, after_main, st, sk)
   if constexpr (VEC == 2 && BM == 128 && BN == 128) {
     if (c_aligned) {
-      if (rk) MYD_LAUNCH(1, true);
-      MYD_LAUNCH(1, false);
+      if (rk) MYD_LAUNCH(true, true);
+      MYD_LAUNCH(true, false);
     }
-#if MYD_OC
-    if ((uintptr_t)C % 8 == 0) {  // unaligned C: realigned 16-byte accesses (CGT 2)
-      if (rk) MYD_LAUNCH(2, true);
-      MYD_LAUNCH(2, false);
-    }
-#endif
   }
-  if (rk) MYD_LAUNCH(0, true);
-  MYD_LAUNCH(0, false);
+  if (rk) MYD_LAUNCH(false, true);
+  MYD_LAUNCH(false, false);
 #undef MYD_LAUNCH
 }
 
