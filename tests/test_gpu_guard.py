@@ -83,7 +83,9 @@ SCRIPT = textwrap.dedent(r"""
         for (m, n, k, lda, ldb, ldc) in cases:
             run(m, n, k, lda, ldb, ldc, at_end=at_end)
             if m > 16 and n > 16:
-                for strips in (2, 4, 8, 16, 32, 34, 36, 40):
+                for strips in (2, 4, 8, 16, 32, 34, 36, 40) + tuple(range(65, 75)):  # + small-block variants
+                    if strips >= 65 and m * n * k > 1e9:
+                        continue
                     run(m, n, k, lda, ldb, ldc, strips=strips, at_end=at_end)
             if m * n * k < 2e8:
                 run(m, n, k, lda, ldb, ldc, exact=True, at_end=at_end)
