@@ -105,6 +105,12 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_L2_PERSIST_MB
 #define MYD_L2_PERSIST_MB 0  // > 0 (with MYD_L2_HINTS): persisting-L2 carve-out for evict_last lines, MB
 #endif
+#ifndef MYD_SPLIT_BOUNDARY
+#define MYD_SPLIT_BOUNDARY 1  // full tiles: half the write-back overlaps the next unit's first slab (0: off)
+#endif
+#ifndef MYD_SB_KSTEPS
+#define MYD_SB_KSTEPS 4  // k-steps of first-half DMMA work the split boundary overlaps with the second half's write-back
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -707,20 +713,21 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   Seg sg;
   bool have = seg_at(cur, sg);
   if (have) g = init_acc(sg, 0);
+  int kt0 = 0;  // slabs of this segment already done (the split boundary runs the first one)
   while (have) {
     const int NS = sg.ke - sg.kb;
     TL_MARK(3);
 #ifdef MYD_FAST_PROFILE
     long long loop_t0 = clock64();
 #endif
-    {
+    if (kt0 < NS) {
       PROF_T0();
-      mbar_wait(&full_bar[g % STAGES], (g / STAGES) & 1);
+      mbar_wait(&full_bar[(g + kt0) % STAGES], ((g + kt0) / STAGES) & 1);
       if (lane == 0) PROF_ADD(4, clock64() - _pt0);
       TL_MARK(4);
+      load_frags(0, (g + kt0) % STAGES, 0);
     }
-    load_frags(0, g % STAGES, 0);
-    for (int kt = 0; kt < NS; ++kt) {
+    for (int kt = kt0; kt < NS; ++kt) {
       const uint32_t gs = g + kt;
       const int slot = gs % STAGES;
       const int nslot = (gs + 1) % STAGES;
@@ -776,6 +783,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     Seg nsg;
     const bool has_next = seg_at(ncur, nsg);
     bool c_loaded = false;  // the next unit's C block already in the accumulators
+    kt0 = 0;
     if (!sg.to_c) {
       store_partial(sg.slot);  // the lower slabs of a tile another CTA finishes
     } else {
@@ -828,32 +836,108 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           const int nrow0 = nsg.m0 + wm * WM + 2 * q, ncol0 = nsg.n0 + wn * WN + r;
           if (!CG && pre)
             for (int cs = 0; cs < CS; ++cs) mbar_wait(&full_bar[(gn + cs) % STAGES], ((gn + cs) / STAGES) & 1);
+          // write back fragment pair (i, i+1) x j of this unit, then (pre) read
+          // the next unit's C into it
+          auto ep_pair = [&](int i, int j) {
+            const double s0 = lo ? acc[i + 1][j][0] : acc[i][j][0];
+            const double s1 = lo ? acc[i + 1][j][1] : acc[i][j][1];
+            const double g0 = __shfl_xor_sync(0xffffffffu, s0, 16);
+            const double g1 = __shfl_xor_sync(0xffffffffu, s1, 16);
+            double *cp = C + (int64_t)(colb + j * 8) * ldc + rowb + i * 8;
+            *reinterpret_cast<double2 *>(cp) = lo ? make_double2(acc[i][j][0], acc[i][j][1]) : make_double2(g0, g1);
+            *reinterpret_cast<double2 *>(cp + 4 * ldc) =
+                lo ? make_double2(g0, g1) : make_double2(acc[i + 1][j][0], acc[i + 1][j][1]);
+            if (pre) {
 #pragma unroll
-          for (int i = 0; i < FM; i += 2)
-#pragma unroll
-            for (int j = 0; j < FN; ++j) {
-              const double s0 = lo ? acc[i + 1][j][0] : acc[i][j][0];
-              const double s1 = lo ? acc[i + 1][j][1] : acc[i][j][1];
-              const double g0 = __shfl_xor_sync(0xffffffffu, s0, 16);
-              const double g1 = __shfl_xor_sync(0xffffffffu, s1, 16);
-              double *cp = C + (int64_t)(colb + j * 8) * ldc + rowb + i * 8;
-              *reinterpret_cast<double2 *>(cp) =
-                  lo ? make_double2(acc[i][j][0], acc[i][j][1]) : make_double2(g0, g1);
-              *reinterpret_cast<double2 *>(cp + 4 * ldc) =
-                  lo ? make_double2(g0, g1) : make_double2(acc[i + 1][j][0], acc[i + 1][j][1]);
-              if (pre) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  if constexpr (CG) {
-                    load_c_pair(i + h, j, nrow0, ncol0, n_inside);
-                  } else {
-                    const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
-                    acc[i + h][j][0] = v.x;
-                    acc[i + h][j][1] = v.y;
-                  }
+              for (int h = 0; h < 2; ++h) {
+                if constexpr (CG) {
+                  load_c_pair(i + h, j, nrow0, ncol0, n_inside);
+                } else {
+                  const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
+                  acc[i + h][j][0] = v.x;
+                  acc[i + h][j][1] = v.y;
                 }
               }
             }
+          };
+          // Split boundary (full tiles, C from global, the next unit a whole
+          // interior tile of >= 2 slabs): write back / reload the first half
+          // of the columns (j < FN/2), run the next unit's first slab on that
+          // half while the second half is written back and reloaded, then
+          // run the same slab on the second half.  Each element still sees
+          // its k-steps in ascending order from C, so C is bitwise unchanged;
+          // the DMMA pipe works through half of the write-back instead of
+          // idling (the boundary is ~7 % of a unit at K = 256).
+          // Phase 2 spans SBS slabs (~MYD_SB_KSTEPS k-steps of first-half DMMA
+          // work); those slabs stay in the ring until the catch-up has used
+          // them.  One slab measured best: 12000^2 x 100 78.0 -> 81.5 %,
+          // 8192^2 x 512 93.2 -> 93.8 %, cfg4 93.3 -> 93.8 %, 8192^3
+          // 98.27 -> 98.37 %; 2-5 slabs gain less (profiles/r02/split_boundary_r02a.log).
+          // The store instructions throttle the warp's issue, so the DMMAs
+          // interleaved with them overlap only part of the write-back.
+          constexpr int SBS = MYD_SB_KSTEPS / KSTEPS > 1 ? MYD_SB_KSTEPS / KSTEPS : 1;
+          constexpr bool SB_OK = MYD_SPLIT_BOUNDARY && CG && !SKM && FN == 4 && (FM / 2) * 2 == FM && STAGES >= SBS + 2;
+          const bool sb = SB_OK && pre && n_inside && nsg.kb == 0 && nsg.ke - nsg.kb >= SBS + 1;
+          if (sb) {
+            if constexpr (SB_OK) {
+              constexpr int FH = FN / 2;
+#pragma unroll
+              for (int i = 0; i < FM; i += 2)
+#pragma unroll
+                for (int j = 0; j < FH; ++j) ep_pair(i, j);
+              const uint32_t g0 = g + NS;  // the next unit's first slab (CG: no C slots)
+              constexpr int NPAIR = (FM / 2) * FH;  // second-half write-back pairs, spread over the k-steps
+              constexpr int NK = SBS * KSTEPS;
+#pragma unroll
+              for (int sl = 0; sl < SBS; ++sl) {
+                const uint32_t gs = g0 + sl;
+                mbar_wait(&full_bar[gs % STAGES], (gs / STAGES) & 1);
+                const double *as0 = smem + (gs % STAGES) * SLOT + a_off;
+                const double *bs0 = smem + (gs % STAGES) * SLOT + A_STAGE + b_off;
+#pragma unroll
+                for (int kk = 0; kk < KSTEPS; ++kk) {
+                  double xa[FM], xb[FH];
+#pragma unroll
+                  for (int i = 0; i < FM; ++i) xa[i] = as0[kk * 4 * AP + i * 8];
+#pragma unroll
+                  for (int j = 0; j < FH; ++j) xb[j] = bs0[kk * 4 + j * 8 * BP];
+#pragma unroll
+                  for (int i = 0; i < FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < FH; ++j) dmma_884(acc[i][j][0], acc[i][j][1], xb[j], xa[i]);
+                  const int ks = sl * KSTEPS + kk;  // (compile-time after unrolling)
+#pragma unroll
+                  for (int t = ks * NPAIR / NK; t < (ks + 1) * NPAIR / NK; ++t) ep_pair(2 * (t / FH), FH + t % FH);
+                }
+              }
+#pragma unroll
+              for (int sl = 0; sl < SBS; ++sl) {
+                const uint32_t gs = g0 + sl;
+                const double *as0 = smem + (gs % STAGES) * SLOT + a_off;
+                const double *bs0 = smem + (gs % STAGES) * SLOT + A_STAGE + b_off;
+#pragma unroll
+                for (int kk = 0; kk < KSTEPS; ++kk) {
+                  double xa[FM], xb[FH];
+#pragma unroll
+                  for (int i = 0; i < FM; ++i) xa[i] = as0[kk * 4 * AP + i * 8];
+#pragma unroll
+                  for (int j = 0; j < FH; ++j) xb[j] = bs0[kk * 4 + (FH + j) * 8 * BP];
+#pragma unroll
+                  for (int i = 0; i < FM; ++i)
+#pragma unroll
+                    for (int j = 0; j < FH; ++j) dmma_884(acc[i][FH + j][0], acc[i][FH + j][1], xb[j], xa[i]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty_bar[gs % STAGES]);
+              }
+              kt0 = SBS;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < FM; i += 2)
+#pragma unroll
+              for (int j = 0; j < FN; ++j) ep_pair(i, j);
+          }
           if (pre) {
             if constexpr (!CG) {
               __syncwarp();
