@@ -873,8 +873,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           // them.  One slab measured best: 12000^2 x 100 78.0 -> 81.5 %,
           // 8192^2 x 512 93.2 -> 93.8 %, cfg4 93.3 -> 93.8 %, 8192^3
           // 98.27 -> 98.37 %; 2-5 slabs gain less (profiles/r02/split_boundary_r02a.log).
-          // The store instructions throttle the warp's issue, so the DMMAs
-          // interleaved with them overlap only part of the write-back.
+          // (Less than the write-back's share of the boundary: the rest of
+          // it -- the reload's latency and the pipeline drain -- stays.)
           constexpr int SBS = MYD_SB_KSTEPS / KSTEPS > 1 ? MYD_SB_KSTEPS / KSTEPS : 1;
           constexpr bool SB_OK = MYD_SPLIT_BOUNDARY && CG && !SKM && FN == 4 && (FM / 2) * 2 == FM && STAGES >= SBS + 2;
           const bool sb = SB_OK && pre && n_inside && nsg.kb == 0 && nsg.ke - nsg.kb >= SBS + 1;
