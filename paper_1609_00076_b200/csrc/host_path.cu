@@ -144,8 +144,30 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   // Program order = issue order: every GEMM is queued right after the
   // uploads it needs, so the device never waits for the host to finish
   // staging unrelated data.
-  if ((e = mv.up(w.dC, dldc, C, ldc, m, nc0)) != cudaSuccess) return capi_cuda_fail(e, "H2D C");
-  for (size_t c = 0; c < kchunks; ++c) {  // group 0: k-chunks as A arrives
+  // The first k-chunk of group 0 runs in column pieces, each as soon as its
+  // C and B land after A's first chunk, so the first GEMM waits for ~1/4 of
+  // group 0's C instead of all of it (column pieces: bitwise the one call).
+  size_t c_first = 0;
+  if (pipelined && kchunks > 1 && nc0 >= 1024) {
+    const int64_t kl = kchunk, piece = ((nc0 / 4) + 127) / 128 * 128;
+    if ((e = mv.up(w.dA, dlda, A, lda, m, kl)) != cudaSuccess) return capi_cuda_fail(e, "H2D A");
+    for (int64_t j0 = 0; j0 < nc0; j0 += piece) {
+      const int64_t nc = std::min<int64_t>(piece, nc0 - j0);
+      if ((e = mv.up(w.dC + j0 * dldc, dldc, C + j0 * ldc, ldc, m, nc)) != cudaSuccess)
+        return capi_cuda_fail(e, "H2D C");
+      if ((e = mv.up(w.dB + j0 * dldb, dldb, B + j0 * ldb, ldb, kl, nc)) != cudaSuccess)
+        return capi_cuda_fail(e, "H2D B");
+      cudaEventRecord(w.ev_in[0], w.s_h2d);  // (each wait takes the record before it)
+      cudaStreamWaitEvent(w.s_comp, w.ev_in[0], 0);
+      e = dispatch(m, (int)nc, (int)kl, w.dA, dlda, w.dB + j0 * dldb, dldb, w.dC + j0 * dldc, dldc, w.s_comp, flags,
+                   ep);
+      if (e != cudaSuccess) return capi_cuda_fail(e, "kernel launch");
+    }
+    c_first = 1;
+  } else if ((e = mv.up(w.dC, dldc, C, ldc, m, nc0)) != cudaSuccess) {
+    return capi_cuda_fail(e, "H2D C");
+  }
+  for (size_t c = c_first; c < kchunks; ++c) {  // group 0: k-chunks as A arrives
     const int64_t p0 = (int64_t)c * kchunk, kl = std::min<int64_t>(kchunk, k - p0);
     if ((e = mv.up(w.dA + p0 * dlda, dlda, A + p0 * lda, lda, m, kl)) != cudaSuccess)
       return capi_cuda_fail(e, "H2D A");
