@@ -521,6 +521,27 @@ def test_blas_alpha_beta_one_is_bitwise_my_dgemm_on_transposed_operands(torch_cu
     assert torch_cuda.equal(c3, c4)
 
 
+@pytest.mark.parametrize("m,n,k,alpha,beta", [(700, 500, 300, -0.75, 2.5), (2048, 2048, 512, 1.0, -3.0),
+                                               (300, 1200, 900, 3.0, 0.5), (256, 256, 256, 2.0, 0.25)])
+def test_blas_beta_folded_into_the_accumulator_start(torch_cuda, m, n, k, alpha, beta):
+    """The reference-BLAS order on the tiled path with beta not in {0, 1}:
+    beta is applied as the kernel loads C (acc = beta * C, Epilogue::cscale)
+    instead of a C := beta C pass, alpha scales the smaller operand -- bitwise
+    the explicit three-step computation (one rounding each)."""
+    torch = torch_cuda
+    a, b, c, _ = dev_operands(torch, m, n, k)
+    got = c.clone()
+    engine.dgemm("N", "N", m, n, k, alpha, a, m, b, k, beta, got, m)
+    want = c * beta
+    if m * k <= k * n:
+        a = a * alpha
+    else:
+        b = b * alpha
+    run_dev(torch, m, n, k, a, m, b, k, want, m)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 @pytest.mark.parametrize("pinned", [False, True])
 def test_host_path_pageable_and_pinned_agree(torch_cuda, pinned):
     """Pageable callers go through the pinned staging ring; pinned ones DMA
