@@ -146,7 +146,7 @@ def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, str
     f |= {0: 0, 1: _capi.FORCE_TILES, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
           16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
           36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
-          **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(11)}}[strips]
+          **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(16)}}[strips]
     return f
 
 
