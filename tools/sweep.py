@@ -52,6 +52,15 @@ def run(name, m, n, k, lda=None, ldb=None, ldc=None, reps=5):
     for _ in range(2):
         go()
     torch.cuda.synchronize()
+    # enough timed reps for >= ~0.4 s under the clock sampler (100 ms period),
+    # so short configs report their SM clock and throttle reasons too
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    go()
+    e1.record()
+    torch.cuda.synchronize()
+    reps = max(reps, min(200, int(0.4 / max(e0.elapsed_time(e1) * 1e-3, 1e-6)) + 1))
     times = []
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
