@@ -137,16 +137,20 @@ def check_conformal(a, b, c) -> tuple[int, int, int]:
     return a.m, b.n, a.n
 
 
+# launch-plan pins of `strips` (dgemm_device) -> flag bits, built once
+_STRIPS_FLAGS = {0: 0, 1: _capi.FORCE_TILES, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
+                 16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
+                 36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
+                 **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(16)}}
+
+
 def _flags(exact: bool, force_tiled: bool = False, force_vec1: bool = False, strips: int = 0,
            path: int | None = None) -> int:
     f = _capi.EXACT if exact else 0
     f |= _capi.FORCE_PATH(path) if path is not None else 0
     f |= _capi.FORCE_TILED if force_tiled else 0
     f |= _capi.FORCE_VEC1 if force_vec1 else 0
-    f |= {0: 0, 1: _capi.FORCE_TILES, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
-          16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
-          36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
-          **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(16)}}[strips]
+    f |= _STRIPS_FLAGS[strips]
     return f
 
 
@@ -252,10 +256,14 @@ def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int
     (1..10; 64: the planner's pick); `path` forces a kernel family
     (_capi.PATH_*, what sharded drivers pass to every shard).  Every plan
     gives bitwise the same C."""
-    lib = _capi.load()
-    _capi.check(lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc,
-                                _flags(exact, force_tiled, force_vec1, strips, path) | _capi.DEVICE_PTRS,
-                                ctypes.c_void_p(stream)))
+    lib = _capi._lib or _capi.load()
+    if exact or force_tiled or force_vec1 or strips or path is not None:
+        flags = _flags(exact, force_tiled, force_vec1, strips, path) | _capi.DEVICE_PTRS
+    else:  # (the common call: no Python work beyond the ctypes call)
+        flags = _capi.DEVICE_PTRS
+    status = lib.my_dgemm_ex(m, n, k, a_ptr, lda, b_ptr, ldb, c_ptr, ldc, flags, stream)
+    if status:
+        _capi.check(status)
 
 
 def fill_random_device(ptr: int, m: int, n: int, ld: int, seed: int, col0: int = 0,
