@@ -143,8 +143,7 @@ int blas_device(char ta, char tb, int m, int n, int k, double alpha, const doubl
   ep.beta = beta;
   ep.blas = !(alpha == 1.0 && beta == 1.0);
   if (fold && ep.blas && beta != 0.0 && path_kind(m, n, flags & ~MY_DGEMM_DEVICE_PTRS) == MY_DGEMM_PATH_TILED) {
-    // beta: folded into the kernel's accumulator start (Epilogue::cscale,
-    // acc = beta * C, the same single rounding as a C := beta C pass)
+    if (beta != 1.0 && (e = launch_scale(m, n, C, ldc, beta, st)) != cudaSuccess) return capi_cuda_fail(e, "scale C");
     if (alpha != 1.0) {
       keep_pool_memory();
       const bool on_a = (int64_t)m * k <= (int64_t)k * n;  // scale the smaller operand
@@ -164,8 +163,7 @@ int blas_device(char ta, char tb, int m, int n, int k, double alpha, const doubl
         return capi_cuda_fail(e, "alpha op");
       }
     }
-    ep = Epilogue{};  // the my_dgemm contract, from beta * C
-    ep.cscale = beta;
+    ep = Epilogue{};  // the my_dgemm contract
   }
   e = dispatch(m, n, k, opA, lda_op, opB, ldb_op, C, ldc, st, flags & ~MY_DGEMM_DEVICE_PTRS, ep);
   return e == cudaSuccess ? capi_ok() : capi_cuda_fail(e, "kernel launch");

@@ -155,10 +155,6 @@ MYD_DEVICE void dmma_884(double &c0, double &c1, double a, double b) {
 struct Epilogue {
   double alpha = 1.0, beta = 1.0;
   int blas = 0;
-  // my_dgemm contract (blas == 0): the accumulator starts at cscale * C.
-  // The BLAS surface folds beta in here instead of a C := beta C pass (one
-  // rounding either way, so bitwise the same); 1.0 is exact.
-  double cscale = 1.0;
 };
 
 // Stream-K schedule of the tiled kernel (iters == 0: unit mode): the first

@@ -625,8 +625,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < FN; ++j) {
         const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gpos, i, j)]);
-        acc[i][j][0] = v.x * ep.cscale;
-        acc[i][j][1] = v.y * ep.cscale;
+        acc[i][j][0] = v.x;
+        acc[i][j][1] = v.y;
       }
     __syncwarp();
     if (lane == 0)
@@ -679,11 +679,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     const double *cp = C + (int64_t)col * ldc + row;
     if (inside) {
       const double2 v = __ldcg(reinterpret_cast<const double2 *>(cp));
-      acc[i][j][0] = v.x * ep.cscale;
-      acc[i][j][1] = v.y * ep.cscale;
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
     } else {
-      acc[i][j][0] = (row < M && col < N) ? __ldcg(cp) * ep.cscale : 0.0;
-      acc[i][j][1] = (row + 1 < M && col < N) ? __ldcg(cp + 1) * ep.cscale : 0.0;
+      acc[i][j][0] = (row < M && col < N) ? __ldcg(cp) : 0.0;
+      acc[i][j][1] = (row + 1 < M && col < N) ? __ldcg(cp + 1) : 0.0;
     }
   };
   auto c_inside = [&](const Seg &s) { return c_aligned && s.m0 + BM <= M && s.n0 + BN <= N; };
@@ -854,8 +854,8 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
                   load_c_pair(i + h, j, nrow0, ncol0, n_inside);
                 } else {
                   const double2 v = *reinterpret_cast<const double2 *>(&smem[c_index(gn, i + h, j)]);
-                  acc[i + h][j][0] = v.x * ep.cscale;
-                  acc[i + h][j][1] = v.y * ep.cscale;
+                  acc[i + h][j][0] = v.x;
+                  acc[i + h][j][1] = v.y;
                 }
               }
             }

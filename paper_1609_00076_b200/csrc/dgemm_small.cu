@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(small::THREADS)
           if (row + 1 < M) v1 = __ldcg(cp + 1);
         }
       }
-      acc[i][j][0] = v0 * ep.cscale;  // (BLAS: beta folded into the start, Epilogue::cscale)
-      acc[i][j][1] = v1 * ep.cscale;
+      acc[i][j][0] = v0;
+      acc[i][j][1] = v1;
     }
 
   const int a_off = q * AP + wm * WM + r;    // + kk*4*AP + i*8

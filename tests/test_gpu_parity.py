@@ -10,6 +10,9 @@ Bars (BASELINE.json north_star):
 
 import ctypes
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -523,11 +526,11 @@ def test_blas_alpha_beta_one_is_bitwise_my_dgemm_on_transposed_operands(torch_cu
 
 @pytest.mark.parametrize("m,n,k,alpha,beta", [(700, 500, 300, -0.75, 2.5), (2048, 2048, 512, 1.0, -3.0),
                                                (300, 1200, 900, 3.0, 0.5), (256, 256, 256, 2.0, 0.25)])
-def test_blas_beta_folded_into_the_accumulator_start(torch_cuda, m, n, k, alpha, beta):
+def test_blas_reference_order_is_bitwise_the_three_steps(torch_cuda, m, n, k, alpha, beta):
     """The reference-BLAS order on the tiled path with beta not in {0, 1}:
-    beta is applied as the kernel loads C (acc = beta * C, Epilogue::cscale)
-    instead of a C := beta C pass, alpha scales the smaller operand -- bitwise
-    the explicit three-step computation (one rounding each)."""
+    C := beta C, alpha scales the smaller operand, then the accumulate
+    contract -- bitwise the explicit three-step computation (one rounding
+    each)."""
     torch = torch_cuda
     a, b, c, _ = dev_operands(torch, m, n, k)
     got = c.clone()

@@ -1,4 +1,4 @@
-"""cfg4 (16384^2 x 256) with three operand sets in one process -- the shape_time.py seeds, the reference generator seeds, A = 0 -- best of 20 single calls each, three rounds (development aid: the time does not depend on the values; the 2-3 % spread of cfg4 between sweep runs is box to box, profiles/r02/cfg4_box_variation_r02a.log)."""
+"""cfg4 (16384^2 x 256) with three operand sets in one process -- the shape_time.py seeds, the reference generator seeds, A = 0 -- best of 20 single calls each, three rounds (development aid: the time does not depend on the values; the 2-3 % cfg4 difference between runs that day was a code regression, profiles/r02/cfg4_box_variation_r02a.log)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
