@@ -111,6 +111,10 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_SB_KSTEPS
 #define MYD_SB_KSTEPS 4  // k-steps of first-half DMMA work the split boundary overlaps with the second half's write-back
 #endif
+#ifndef MYD_ROUND_SYNC
+#define MYD_ROUND_SYNC 0  // default of MY_DGEMM_ROUND_SYNC (rounds between re-alignments of long-K calls; 0 = off):
+                          // cfg5 DRAM reads 722 -> 417 GB but +0.3 % time (profiles/r02/round_sync_r02b.log)
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -191,7 +195,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, bool RS = false>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -410,6 +414,33 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     bool first_seg = true;
     for (; have; cur = seg_next(cur, sg), have = seg_at(cur, sg), first_seg = false) {
       const int m0 = sg.m0, n0 = sg.n0;
+      if constexpr (RS && !SKM) {
+        // Round re-alignment (its own instantiation, long-K whole-tile
+        // launches only, co-resident grid): before the first slab of round w
+        // (a multiple of R = sk.iters, below sk.dp_tiles whole rounds) the CTA
+        // arrives on the zeroed counter sk.flags[0] and waits for all of
+        // them; only producer warp 0 waits -- no slab of the round completes
+        // without its arrival, so the whole CTA follows.  Over a 1.9 s cfg5
+        // call the CTAs otherwise drift apart in K and read shared panel
+        // slabs from HBM once per drifted sharer instead of once per round
+        // (profiles/r02/dram_drift_r02a.log).
+        if (pw == 0) {
+          const int w = cur / (int)gridDim.x, R = (int)sk.iters;
+          if (w > 0 && w < (int)sk.dp_tiles && w % R == 0) {
+            if (lane == 0) {
+              atomicAdd(sk.flags, 1ull);
+              const unsigned long long target = (unsigned long long)(w / R) * gridDim.x;
+              for (;;) {
+                unsigned long long v;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(sk.flags) : "memory");
+                if (v >= target) break;
+                __nanosleep(200);
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
 #ifdef MYD_TIMELINE
       if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg) g_tl[9] = gtimer();
 #endif
@@ -999,7 +1030,7 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, bool RS = false>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -1015,9 +1046,8 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)MYD_L2_PERSIST_MB << 20);
       cudaGetLastError();
     }
-    cudaError_t e =
-        cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Ring<BM, BN, BK>::BYTES);
+    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
   }
@@ -1028,13 +1058,15 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = Ring<BM, BN, BK>::BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK>, M, N, K, A, lda, B, ldb, C, ldc,
-                                     tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
+  attr[1].id = cudaLaunchAttributeCooperative;  // RS: the round re-alignment needs every CTA resident
+  attr[1].val.cooperative = 1;
+  cfg.attrs = pdl_enabled() ? attr : attr + 1;
+  cfg.numAttrs = (pdl_enabled() ? 1 : 0) + (RS ? 1 : 0);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS>, M, N, K, A, lda, B, ldb,
+                                     C, ldc, tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -1060,6 +1092,16 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
                                                         tile0, edge, after_main, st, sk)
   if constexpr (VEC == 2 && BM == 128 && BN == 128) {
     if (c_aligned) {
+      if constexpr (BK == 32 && !SKM) {
+        if (sk.iters > 0 && sk.flags) {  // round re-alignment (RoundSync)
+          cudaError_t e = rk ? launch_kernel<VEC, BM, BN, BK, SKM, true, true, true>(
+                                   ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st, sk)
+                             : launch_kernel<VEC, BM, BN, BK, SKM, true, false, true>(
+                                   ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st, sk);
+          if (e == cudaSuccess) return e;
+          cudaGetLastError();  // no co-resident launch here: the plain instantiation, without re-alignment
+        }
+      }
       if (rk) MYD_LAUNCH(true, true);
       MYD_LAUNCH(true, false);
     }
@@ -1073,12 +1115,12 @@ template <int VEC>
 cudaError_t launch_split(const Epilogue &ep, int split, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                          const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
                          int after_main,
-                         cudaStream_t st) {
+                         cudaStream_t st, const StreamK &rs = StreamK{}) {
   switch (split) {  // units per 128x128 tile
     case 1:
       if constexpr (VEC == 2) {
-        if (K >= MYD_BK32_MIN_K)  // long K: deeper slabs, fewer ring handshakes
-          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
+        if (K >= MYD_BK32_MIN_K)  // long K: deeper slabs, fewer ring handshakes (rs: round re-alignment)
+          return launch_one<VEC, 128, 128, 32>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st, rs);
       }
       return launch_one<VEC, 128, 128, 16>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
     case 2: return launch_one<VEC, 128, 64>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st);
@@ -1171,6 +1213,43 @@ cudaError_t launch_streamk_split(const Epilogue &ep, int split, int M, int N, in
 }
 
 std::atomic<int> g_max_ctas{0};  // my_dgemm_set_max_ctas: 0 = every SM
+
+// Round re-alignment of long-K whole-tile launches (MY_DGEMM_ROUND_SYNC=R,
+// default MYD_ROUND_SYNC: every R rounds; 0 = off; only K >= 16384, where a
+// call lasts long enough for the CTAs to drift): a zeroed counter from the
+// stream-ordered pool, passed in the unit-mode launch's unused StreamK fields
+// (flags = counter, iters = R, dp_tiles = whole rounds).
+int round_sync_rounds() {
+  static const int r = [] {
+    const char *v = getenv("MY_DGEMM_ROUND_SYNC");
+    return v && *v ? atoi(v) : MYD_ROUND_SYNC;
+  }();
+  return r;
+}
+struct RoundSync {
+  unsigned long long *ctr = nullptr;
+  StreamK sk;
+  cudaError_t setup(long long units, long long G, bool ragged, int K, cudaStream_t st) {
+    const int R = round_sync_rounds();
+    if (R <= 0 || ragged || K < 16384 || units / G < 2LL * R) return cudaSuccess;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;  // (no cooperative launch inside a capture)
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return cudaSuccess;
+    }
+    keep_pool_memory_fast();
+    cudaError_t e = cudaMallocAsync((void **)&ctr, sizeof(*ctr), st);
+    if (e != cudaSuccess) return e;
+    sk.flags = ctr;
+    sk.iters = R;
+    sk.dp_tiles = units / G;
+    return cudaMemsetAsync(ctr, 0, sizeof(*ctr), st);
+  }
+  void release(cudaStream_t st) {
+    if (ctr) cudaFreeAsync(ctr, st);
+    ctr = nullptr;
+  }
+};
 
 // SMs the persistent grid may occupy: the device's count, or fewer when the
 // caller reserves SMs for concurrent work (e.g. NCCL kernels of an
@@ -1409,11 +1488,16 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // whole-tile rounds for all but the last one-to-two waves in the unit-mode
     // kernel, then the stream-K phase as a tail launch (its own tiles only)
     const long long dp_tiles = (tiles / G - 1) * G;
-    if (dp_tiles > 0)
-      e = vec2 ? launch_split<2>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
-                                 stream)
-               : launch_split<1>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
-                                 stream);
+    RoundSync rsync;
+    if (dp_tiles > 0) {
+      e = rsync.setup(dp_tiles, G, M % TILE_M != 0 || N % TILE_N != 0, K, stream);
+      if (e == cudaSuccess)
+        e = vec2 ? launch_split<2>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
+                                   stream, rsync.sk)
+                 : launch_split<1>(ep, 1, (unsigned)dp_tiles, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0, 0,
+                                   stream, rsync.sk);
+    }
+    rsync.release(stream);
     if (e == cudaSuccess)
       e = vec2 ? launch_streamk_split<2>(ep, 1, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, dp_tiles,
                                          dp_tiles > 0, stream, ws.sk)

@@ -340,6 +340,43 @@ def test_small_kernel_bitwise_equals_units(torch_cuda, m, n, k, lda, ldb, ldc):
         assert np.all(ref.cpu().numpy().reshape(n, ldc)[:, m:] == -777.25)
 
 
+_ROUND_SYNC_RUN = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, {repo!r})
+from paper_1609_00076_b200 import engine
+m, n, k = 8192, 8192, 16384
+st = torch.cuda.current_stream().cuda_stream
+ops = [torch.empty(r * c, dtype=torch.float64, device="cuda") for r, c in ((m, k), (k, n), (m, n))]
+for t, (buf, r, c) in enumerate(zip(ops, (m, k, m), (k, n, n))):
+    engine.fill_random_device(buf.data_ptr(), r, c, r, 77 + t, 0, st)
+engine.dgemm_device(m, n, k, ops[0].data_ptr(), m, ops[1].data_ptr(), k, ops[2].data_ptr(), m, st)
+np.save(sys.argv[1], ops[2][: 64 * m].cpu().numpy())  # (enough to compare: the first 64 columns)
+np.save(sys.argv[1] + ".sum.npy", np.array([float(ops[2].sum()), float(ops[2].abs().sum())]))
+"""
+
+
+def test_round_realignment_changes_timing_never_results(torch_cuda, tmp_path):
+    """MY_DGEMM_ROUND_SYNC: long-K whole-tile launches re-align their rounds
+    on a grid counter every R rounds (own instantiation, cooperative launch);
+    C is bitwise the unsynchronised run (8192^2 x 16384: 25 whole rounds,
+    R = 4 -> 5 re-alignments)."""
+    import subprocess
+
+    script = tmp_path / "run.py"
+    script.write_text(_ROUND_SYNC_RUN.format(repo=os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+    outs, sums = [], []
+    for r in ("0", "4"):
+        out = tmp_path / f"c{r}.npy"
+        env = dict(os.environ, MY_DGEMM_ROUND_SYNC=r)
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=600)
+        outs.append(np.load(out))
+        sums.append(np.load(str(out) + ".sum.npy"))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(sums[0], sums[1])
+
+
 def test_fast_deterministic(torch_cuda):
     m, n, k = 1000, 1100, 1200
     a, b, c, _ = dev_operands(torch_cuda, m, n, k)
