@@ -108,9 +108,46 @@ __global__ void __launch_bounds__(small::THREADS)
     }
   };
 
+  // Full slabs of an interior block (no bounds, whole 16 / 8-byte chunks):
+  // each thread's chunks sit at fixed offsets that advance by a constant
+  // per pass, so a slab costs a few instructions per cp.async instead of the
+  // bounds arithmetic above -- with one warp per sub-partition those
+  // instructions sit between the DMMAs of the K chain.
+  constexpr int A_CPR = BM / VEC, B_CPC = BK / VEC;  // chunks per A k-row / per B column
+  static_assert(THREADS % A_CPR == 0 && (THREADS % B_CPC == 0 || B_CPC % THREADS == 0), "chunk passes");
+  constexpr int A_ROWS_PP = THREADS / A_CPR, A_PASSES = BK / A_ROWS_PP;
+  constexpr int B_COLS_PP = THREADS >= B_CPC ? THREADS / B_CPC : 1, B_PASSES = BK * BN / VEC / THREADS;
+  const bool interior = m0 + BM <= M && n0 + BN <= N;
+  const int a_kk0 = tid / A_CPR, a_mm0 = (tid % A_CPR) * VEC;
+  const int b_nn0 = tid / B_CPC, b_kk0 = (tid % B_CPC) * VEC;
+  const double *const a_base = A + (int64_t)a_kk0 * lda + m0 + a_mm0;
+  const double *const b_base = B + (int64_t)(n0 + b_nn0) * ldb + b_kk0;
+  auto load_slab_fast = [&](int slot, int kt) {
+    double *as = smem + slot * SLOT + a_kk0 * AP + a_mm0;
+    double *bs = smem + slot * SLOT + A_ST + b_nn0 * BP + b_kk0;
+    const double *pa = a_base + (int64_t)kt * BK * lda;
+    const double *pb = b_base + kt * BK;
+#pragma unroll
+    for (int c = 0; c < A_PASSES; ++c) cp_async<VEC * 8>(as + c * A_ROWS_PP * AP, pa + (int64_t)c * A_ROWS_PP * lda, VEC * 8);
+#pragma unroll
+    for (int c = 0; c < B_PASSES; ++c) {
+      if constexpr (THREADS >= B_CPC) {
+        cp_async<VEC * 8>(bs + c * B_COLS_PP * BP, pb + (int64_t)c * B_COLS_PP * ldb, VEC * 8);
+      } else {  // a column takes several passes
+        constexpr int PPC = B_CPC / THREADS;  // passes per column
+        cp_async<VEC * 8>(bs + (c / PPC) * BP + (c % PPC) * THREADS * VEC,
+                          pb + (int64_t)(c / PPC) * ldb + (c % PPC) * THREADS * VEC, VEC * 8);
+      }
+    }
+  };
+  auto issue_slab = [&](int slot, int kt) {
+    if (interior && (kt + 1) * BK <= K) load_slab_fast(slot, kt);
+    else load_slab(slot, kt);
+  };
+
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_slab(s, s);
+    if (s < KT) issue_slab(s, s);
     cp_async_commit();
   }
 
@@ -158,17 +195,20 @@ __global__ void __launch_bounds__(small::THREADS)
   for (int kt = 0; kt < KT; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();  // slab kt landed for every thread; slot (kt - 1) % STAGES free
-    {
-      const int nk = kt + STAGES - 1;
-      if (nk < KT) load_slab(nk % STAGES, nk);
-      cp_async_commit();
-    }
+    const int nk = kt + STAGES - 1;
     const double *as = smem + (kt % STAGES) * SLOT;
     const double *bs = as + A_ST;
     if (kt + 1 < KT || K % BK == 0) {
+      // the next slab's copies go out after the first k-step, so the chain
+      // restarts at once after the barrier
+      kstep(as, bs, 0);
+      if (nk < KT) issue_slab(nk % STAGES, nk);
+      cp_async_commit();
 #pragma unroll
-      for (int kk = 0; kk < KSTEPS; ++kk) kstep(as, bs, kk);
+      for (int kk = 1; kk < KSTEPS; ++kk) kstep(as, bs, kk);
     } else {
+      if (nk < KT) issue_slab(nk % STAGES, nk);
+      cp_async_commit();
       // last slab of a ragged K: only the k-groups holding some k < K
       const int nsteps = (K - kt * BK + 3) / 4;
 #pragma unroll
