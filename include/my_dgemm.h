@@ -60,6 +60,22 @@ extern "C" {
 #define MY_DGEMM_SMALL_VARIANT(v) ((unsigned)(v) << 14)
 #define MY_DGEMM_SMALL_MASK 0x3C000u
 #define MY_DGEMM_FORCE_TILES 0x40000u /* every tile as a full 128x128 tile (tests, tuner: plan 1) */
+/* Every launch plan of the tiled path but one gives each element of C the same
+ * ascending chain of k-steps, so C is bitwise independent of the plan, of
+ * k-chunking at multiples of 16 and of the shard count.  The exception is the
+ * opt-in K-split plan (plan 48) for problems with fewer 128x128 tiles than
+ * SMs: a tile's K range is cut into pieces that run on several SMs at once
+ * and whose partial sums the tile's owner adds in a fixed order -- still
+ * deterministic (a function of m, n, k and the SM count) and within the
+ * stated tolerance, but not that chain.  It runs only when asked for:
+ * MY_DGEMM_FORCE_KSPLIT on the call (when the shape allows it; otherwise the
+ * heuristic's plan-invariant choice), or MY_DGEMM_KSPLIT=1 in the environment,
+ * which lets the planner cost it against the other plans (off by default: it
+ * measured no faster).  MY_DGEMM_PLAN_INVARIANT keeps a call to
+ * the plan-invariant plans even then; MY_DGEMM_FORCE_PATH (sharded drivers),
+ * an SM cap, a pinned plan and the host path's panel pipeline imply it. */
+#define MY_DGEMM_PLAN_INVARIANT 0x80000u
+#define MY_DGEMM_FORCE_KSPLIT 0x100000u
 /* Run this call on kernel family p (MY_DGEMM_PATH_*, see my_dgemm_path) whatever
  * the shape's own choice would be: sharded drivers pass the whole problem's
  * path to every shard so C is bitwise independent of the shard count.  The

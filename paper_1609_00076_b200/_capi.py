@@ -27,6 +27,8 @@ FORCE_STREAMK = 0x800
 BLAS_EPILOGUE = 0x1000
 FORCE_SMALL = 0x2000
 FORCE_TILES = 0x40000
+PLAN_INVARIANT = 0x80000
+FORCE_KSPLIT = 0x100000
 
 
 def SMALL_VARIANT(v: int) -> int:  # noqa: N802 - mirrors the C macro

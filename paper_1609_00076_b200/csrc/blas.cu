@@ -199,7 +199,7 @@ extern "C" int my_dgemm_blas(char transa, char transb, int m, int n, int k, doub
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
                          MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_FORCE_STREAMK | MY_DGEMM_PATH_MASK |
-                         MY_DGEMM_BLAS_EPILOGUE;
+                         MY_DGEMM_BLAS_EPILOGUE | MY_DGEMM_PLAN_INVARIANT | MY_DGEMM_FORCE_KSPLIT;
   if (flags & ~known) return capi_fail(-14, "unknown flag bits");
   const bool fold = !(flags & MY_DGEMM_BLAS_EPILOGUE);
   flags &= ~MY_DGEMM_BLAS_EPILOGUE;

@@ -120,7 +120,10 @@ cudaError_t dispatch(int m, int n, int k, const double *A, int64_t lda, const do
   if (flags & MY_DGEMM_FORCE_STREAMK) split = 32 + (split == 16 ? 0 : split);  // stream-K over those units
   if (flags & MY_DGEMM_FORCE_SMALL) split = 64 + (int)((flags & MY_DGEMM_SMALL_MASK) >> 14);  // small-block kernel
   if (flags & MY_DGEMM_FORCE_TILES) split = 1;  // full tiles only
+  if (flags & MY_DGEMM_FORCE_KSPLIT) split = 48;  // K-split plan (when the shape allows it)
   if (split == 0) split = tuned_plan(m, n, k, lda, ldb);  // 0 unless my_dgemm_tune chose one
+  // sharded drivers (forced path) and callers asking for it: heuristic over the plan-invariant plans only
+  if (split == 0 && (flags & (MY_DGEMM_PATH_MASK | MY_DGEMM_PLAN_INVARIANT))) split = -1;
   const bool force_vec1 = (flags & MY_DGEMM_FORCE_VEC1) != 0;
   const bool a_ok = lda % 2 == 0 && (uintptr_t)A % 16 == 0, b_ok = ldb % 2 == 0 && (uintptr_t)B % 16 == 0;
   // Worth a scratch copy when the GEMM is big, or when its K chain is long:
@@ -251,7 +254,8 @@ int my_dgemm_ex(int m, int n, int k, const double *A, int lda, const double *B, 
   const unsigned known = MY_DGEMM_DEVICE_PTRS | MY_DGEMM_EXACT | MY_DGEMM_FORCE_TILED | MY_DGEMM_FORCE_VEC1 |
                          MY_DGEMM_FORCE_STRIPS2 | MY_DGEMM_FORCE_STRIPS4 | MY_DGEMM_FORCE_UNITS8 |
                          MY_DGEMM_FORCE_ROWS16 | MY_DGEMM_FORCE_STREAMK | MY_DGEMM_PATH_MASK | MY_DGEMM_FORCE_SMALL |
-                         MY_DGEMM_SMALL_MASK | MY_DGEMM_FORCE_TILES;
+                         MY_DGEMM_SMALL_MASK | MY_DGEMM_FORCE_TILES | MY_DGEMM_PLAN_INVARIANT |
+                         MY_DGEMM_FORCE_KSPLIT;
   if (flags & ~known) return fail(-10, "unknown flag bits");
   if (!path_fits(m, n, flags)) return fail(-10, "MY_DGEMM_FORCE_PATH does not suit the shape");
   if (flags & MY_DGEMM_DEVICE_PTRS) {

@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -70,6 +71,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #else
 #define TL_MARK(i) do { } while (0)
+#endif
+#ifdef MYD_KS_TIMELINE
+// Stream-K / K-split launches: globaltimer marks of every CTA's consumer warp 0
+// (tools/ksplit_timeline.py): [15] entry, [14] exit; per segment s (5 s + ..):
+// +0 accumulators ready, +1 K loop done, +2 partial stored / fix-up done,
+// +3 C stored, +4 next accumulators ready
+__device__ unsigned long long g_kst[160][16];
+#define KST(i)                                                                       \
+  do {                                                                               \
+    if (SKM && warp == 0 && lane == 0 && (i) < 16) {                                 \
+      unsigned long long _t;                                                         \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t));                          \
+      g_kst[blockIdx.x % 160][i] = _t;                                               \
+    }                                                                                \
+  } while (0)
+#else
+#define KST(i) do { } while (0)
 #endif
 #ifdef MYD_FAST_PROFILE
 // [0] consumer slow-wait cycles, [1] consumer slow waits, [2] producer empty-wait cycles,
@@ -114,6 +132,9 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_ROUND_SYNC
 #define MYD_ROUND_SYNC 0  // default of MY_DGEMM_ROUND_SYNC (rounds between re-alignments of long-K calls; 0 = off):
                           // cfg5 DRAM reads 722 -> 417 GB but +0.3 % time (profiles/r02/round_sync_r02b.log)
+#endif
+#ifndef MYD_KSPLIT_FIXUP_US
+#define MYD_KSPLIT_FIXUP_US 2.5  // K-split plan: owner's fix-up cost per piece of a tile (us, planner model)
 #endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
@@ -195,7 +216,7 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, bool RS = false>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -302,6 +323,19 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // least one tile per CTA, so a tile is cut at most once, and CTA b only
   // ever waits for CTA b + 1's first segment (which waits on nothing): no
   // deadlock.  Cursor: < SK0 a data-parallel tile, else SK0 + iteration.
+  //
+  // K-split mode (SUM, its own instantiation; fewer tiles than CTAs, so a
+  // CTA's range is shorter than a tile and a tile is cut into several pieces):
+  // the same even split, but the pieces of a tile are independent.  The piece
+  // holding the top slab (the end of CTA b's range) is the owner: it starts
+  // from C and, after its slabs, adds the partial sums of the tile's other
+  // pieces -- each accumulated from zero by CTAs b + 1, b + 2, ... as the
+  // first segment of their ranges (so they are done, or finish together with
+  // the owner) -- in CTA order, then stores C.  No piece waits before its
+  // slabs, so the K chain of a tile runs on several SMs at once; each element
+  // is a fixed function of (m, n, k, CTA count), but no longer the single
+  // ascending chain of the other plans (launch_dgemm_fast: only chosen when
+  // the caller has not asked for plan-invariant results).
   struct Seg {
     int m0, n0, kb, ke, slot;
     bool from_c, to_c;
@@ -336,9 +370,14 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       unit_origin((int)sk.tile0 + t, sg.m0, sg.n0);
       sg.kb = KT - l1;
       sg.ke = KT - l0;
-      sg.from_c = sg.kb == 0;
       sg.to_c = sg.ke == KT;
-      sg.slot = sg.to_c ? (int)blockIdx.x : (int)blockIdx.x - 1;  // upper part reads b; lower part writes b - 1
+      if constexpr (SUM) {
+        sg.from_c = sg.to_c;          // the owner starts from C, the other pieces from zero
+        sg.slot = (int)blockIdx.x;    // a CTA's only non-owner piece is the first of its range
+      } else {
+        sg.from_c = sg.kb == 0;
+        sg.slot = sg.to_c ? (int)blockIdx.x : (int)blockIdx.x - 1;  // upper part reads b; lower part writes b - 1
+      }
       return true;
     }
   };
@@ -673,20 +712,25 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   auto part_base = [&](int slot) -> double2 * {
     return reinterpret_cast<double2 *>(sk.work) + ((int64_t)slot * CONSUMER_WARPS + warp) * NV2 * 32 + lane;
   };
+  // (two steps: the stores are issued, the caller starts loading the next
+  // segment's accumulators, and only then does the flag go out -- its release,
+  // cumulative over the warp's stores through the warp barrier, waits for them
+  // while the loads are already in flight)
   auto store_partial = [&](int slot) {
     double2 *p = part_base(slot);
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
       for (int j = 0; j < FN; ++j) __stcg(p + (i * FN + j) * 32, make_double2(acc[i][j][0], acc[i][j][1]));
-    __threadfence();
+  };
+  auto publish_partial = [&](int slot) {
     __syncwarp();
     if (lane == 0)
       asm volatile("st.release.gpu.global.u64 [%0], %1;\n" ::"l"(sk.flags + slot * CONSUMER_WARPS + warp),
                    "l"(sk.epoch)
                    : "memory");
   };
-  auto load_partial = [&](int slot) {
+  auto wait_partial = [&](int slot) {
     const unsigned long long *f = sk.flags + slot * CONSUMER_WARPS + warp;
     for (;;) {
       unsigned long long v;
@@ -694,6 +738,29 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       if (v == sk.epoch) break;
       __nanosleep(64);
     }
+  };
+  // K-split: acc += the partial sums in workspace slot `slot`
+  // (loads in batches of PB, all in flight before the first add: with the
+  // compiler's 4 per batch a 128 KB partial took ~2.5 us of L2 round trips)
+  [[maybe_unused]] auto add_partial = [&](int slot) {
+    wait_partial(slot);
+    const double2 *p = part_base(slot);
+    constexpr int PB = NV2 < 16 ? NV2 : 16;
+#pragma unroll
+    for (int v0 = 0; v0 < NV2; v0 += PB) {
+      double2 t[PB];
+#pragma unroll
+      for (int v = 0; v < PB; ++v)
+        asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];\n" : "=d"(t[v].x), "=d"(t[v].y) : "l"(p + (v0 + v) * 32));
+#pragma unroll
+      for (int v = 0; v < PB; ++v) {
+        acc[(v0 + v) / FN][(v0 + v) % FN][0] += t[v].x;
+        acc[(v0 + v) / FN][(v0 + v) % FN][1] += t[v].y;
+      }
+    }
+  };
+  auto load_partial = [&](int slot) {
+    wait_partial(slot);
     const double2 *p = part_base(slot);
 #pragma unroll
     for (int i = 0; i < FM; ++i)
@@ -723,7 +790,14 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   // ring position gpos; returns the ring position of its first slab
   auto init_acc = [&](const Seg &sg, uint32_t gpos) -> uint32_t {
     if (!sg.from_c) {
-      load_partial(sg.slot);
+      if constexpr (SUM) {  // a K-split piece that does not own the tile: partial sums from zero
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      } else {
+        load_partial(sg.slot);
+      }
       return gpos;
     }
     if constexpr (CG) {
@@ -743,11 +817,14 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
   int cur = seg_first();
   Seg sg;
   bool have = seg_at(cur, sg);
+  KST(15);
   if (have) g = init_acc(sg, 0);
+  [[maybe_unused]] int seg_ord = 0;
   int kt0 = 0;  // slabs of this segment already done (the split boundary runs the first one)
   while (have) {
     const int NS = sg.ke - sg.kb;
     TL_MARK(3);
+    KST(seg_ord * 5);
 #ifdef MYD_FAST_PROFILE
     long long loop_t0 = clock64();
 #endif
@@ -809,6 +886,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     }
 #endif
     TL_MARK(5);
+    KST(seg_ord * 5 + 1);
     // the next segment (worked out after the K loop: nothing extra stays live in it)
     const int ncur = seg_next(cur, sg);
     Seg nsg;
@@ -816,8 +894,21 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     bool c_loaded = false;  // the next unit's C block already in the accumulators
     kt0 = 0;
     if (!sg.to_c) {
-      store_partial(sg.slot);  // the lower slabs of a tile another CTA finishes
+      store_partial(sg.slot);  // the lower slabs of a tile another CTA finishes (published below)
+      KST(seg_ord * 5 + 2);
     } else {
+      if constexpr (SKM && SUM) {
+        // K-split owner of a cut tile: the other pieces' partial sums, in CTA
+        // order (CTAs b + 1, ... whose range starts inside this tile)
+        if (cur >= SK0 && sg.kb > 0) {
+          const int tile_end = ((cur - SK0) / KT + 1) * KT;
+          for (int b2 = (int)blockIdx.x + 1; b2 < (int)gridDim.x; ++b2) {
+            if (sk_per * b2 + min(b2, sk_rem) >= tile_end) break;
+            add_partial(b2);
+          }
+        }
+      }
+      KST(seg_ord * 5 + 2);
       // Accumulator map (the DMMA computes the C^T block, B^T A^T, so each
       // thread's pair is two consecutive rows of one column: 16 contiguous
       // bytes in column-major C):  acc[i][j][e] = C(row0 + 8i + e, col0 + 8j).
@@ -999,8 +1090,16 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           }
         }
     }
+    KST(seg_ord * 5 + 3);
     g += NS;
+    // (a next segment that itself starts from another CTA's partial waits for
+    // it: publish first, or the waits would chain from CTA to CTA)
+    const bool publish_first = !sg.to_c && !SUM && has_next && !nsg.from_c;
+    if (publish_first) publish_partial(sg.slot);
     if (has_next) g = c_loaded ? g + CSR : init_acc(nsg, g);
+    if (!sg.to_c && !publish_first) publish_partial(sg.slot);
+    KST(seg_ord * 5 + 4);
+    ++seg_ord;
     TL_MARK(6);
 #ifdef MYD_TIMELINE
     ++unit_ord;
@@ -1009,6 +1108,7 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
     sg = nsg;
     have = has_next;
   }
+  KST(14);
   if (after_main) asm volatile("griddepcontrol.wait;\n" ::: "memory");
 #ifdef MYD_TIMELINE
   if (tid == 0) atomicMax(&g_tl[1], gtimer());
@@ -1030,7 +1130,7 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, bool RS = false>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -1046,7 +1146,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)MYD_L2_PERSIST_MB << 20);
       cudaGetLastError();
     }
-    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS>,
+    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
@@ -1065,7 +1165,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   attr[1].val.cooperative = 1;
   cfg.attrs = pdl_enabled() ? attr : attr + 1;
   cfg.numAttrs = (pdl_enabled() ? 1 : 0) + (RS ? 1 : 0);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS>, M, N, K, A, lda, B, ldb,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM>, M, N, K, A, lda, B, ldb,
                                      C, ldc, tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
@@ -1077,7 +1177,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
 // ring-staged one, whose 8-byte staging copies hide the latency scalar global
 // loads would expose (16384^2 x 256, ldc odd: 5.43 ms -> 4.45 ms).  A runtime
 // switch inside one kernel cost the aligned case 2-10 %.
-template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>(), bool SKM = false>
+template <int VEC, int BM, int BN, int BK = fast::default_bk<BM, BN>(), bool SKM = false, bool SUM = false>
 cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                        const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                        int edge, int after_main, cudaStream_t st, const StreamK &sk = StreamK{}) {
@@ -1088,8 +1188,8 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   // depend on the plan or on which kernel a shard's tile lands in.
   const bool rk = MYD_SKIP_ZERO_KSTEPS && K % BK != 0 && BK - K % BK >= 4;
 #define MYD_LAUNCH(CGT_, RK_)                                                                                   \
-  return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, \
-                                                        tile0, edge, after_main, st, sk)
+  return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_, false, SUM>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, \
+                                                                    tiles_n, tile0, edge, after_main, st, sk)
   if constexpr (VEC == 2 && BM == 128 && BN == 128) {
     if (c_aligned) {
       if constexpr (BK == 32 && !SKM) {
@@ -1149,21 +1249,90 @@ inline void keep_pool_memory_fast() { keep_pool_memory(); }
 // match.
 std::atomic<unsigned long long> g_sk_epochs{0};
 
-// Workspace of one stream-K call: one partial unit per CTA plus per-warp
-// flags, from the stream-ordered pool, flags zeroed (before the call's first
-// launch, so the stream-K launch still follows its predecessor by PDL).
-struct SkWorkspace {
+// Workspace of one stream-K / K-split call: one partial unit per CTA plus
+// per-warp flags.  Normally a block owned by the call's stream (up to
+// SK_STREAMS streams per device, keyed by cudaStreamGetId, allocated and its
+// flags zeroed once, never freed): calls on one stream run in order -- a PDL
+// successor touches global memory only after its griddepcontrol.wait, i.e.
+// after the previous grid has completed -- and every launch has its own epoch,
+// so flags left by earlier calls never match and nothing has to be zeroed or
+// allocated per call (the memset between two kernels also kept the launch from
+// overlapping its predecessor: 896^3 stream-K 59.1 -> 53.6 us, 1280^3
+// 138.8 -> 133.8 us, profiles/r02/ksplit_r02b.log).  During stream capture, with more streams
+// than slots, or when the allocation fails: a block from the stream-ordered
+// pool, flags zeroed by a memset node ahead of the launch, freed after it.
+constexpr int SK_STREAMS = 8;
+struct SkOwned {
+  unsigned long long stream_id = 0;
   void *base = nullptr;
+  size_t ctas = 0;
+};
+struct SkDevice {
+  std::mutex mu;
+  SkOwned own[SK_STREAMS];
+  int n = 0;
+};
+SkDevice g_sk_dev[64];
+
+struct SkWorkspace {
+  void *base = nullptr;  // pooled block (freed by release), else nullptr
   StreamK sk;
-  cudaError_t alloc(int G, cudaStream_t st) {
-    const size_t part = (size_t)G * fast::CONSUMER_WARPS * 32 * 64 * 8, flags = (size_t)G * fast::CONSUMER_WARPS * 8;
-    keep_pool_memory_fast();
-    cudaError_t e = cudaMallocAsync(&base, part + flags, st);
-    if (e != cudaSuccess) return e;
-    sk.work = static_cast<double *>(base);
-    sk.flags = reinterpret_cast<unsigned long long *>(static_cast<char *>(base) + part);
+  static constexpr size_t part_bytes(size_t G) { return G * fast::CONSUMER_WARPS * 32 * 64 * 8; }
+  static constexpr size_t flag_bytes(size_t G) { return G * fast::CONSUMER_WARPS * 8; }
+  void point(void *b, size_t G) {
+    sk.work = static_cast<double *>(b);
+    sk.flags = reinterpret_cast<unsigned long long *>(static_cast<char *>(b) + part_bytes(G));
     sk.epoch = 0x5DA7000000000000ull | (g_sk_epochs.fetch_add(1) + 1);
-    return cudaMemsetAsync(sk.flags, 0, flags, st);
+  }
+  bool owned(int G, cudaStream_t st) {
+    static const bool off = [] {  // MY_DGEMM_SK_POOLED=1: always the pooled block (A/B timing)
+      const char *v = getenv("MY_DGEMM_SK_POOLED");
+      return v && *v && *v != '0';
+    }();
+    if (off) return false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    unsigned long long id = 0;
+    int dev = 0;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone ||
+        cudaStreamGetId(st, &id) != cudaSuccess || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+      cudaGetLastError();
+      return false;
+    }
+    SkDevice &d = g_sk_dev[dev];
+    std::lock_guard<std::mutex> lock(d.mu);
+    for (int i = 0; i < d.n; ++i)
+      if (d.own[i].stream_id == id) {
+        if (d.own[i].ctas < (size_t)G) return false;
+        point(d.own[i].base, d.own[i].ctas);
+        return true;
+      }
+    if (d.n >= SK_STREAMS) return false;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t ctas = (size_t)std::max(G, sms);
+    void *b = nullptr;
+    if (cudaMalloc(&b, part_bytes(ctas) + flag_bytes(ctas)) != cudaSuccess ||
+        cudaMemset(static_cast<char *>(b) + part_bytes(ctas), 0, flag_bytes(ctas)) != cudaSuccess) {
+      cudaGetLastError();
+      if (b) cudaFree(b);
+      return false;
+    }
+    d.own[d.n++] = SkOwned{id, b, ctas};
+    point(b, ctas);
+    return true;
+  }
+  cudaError_t alloc(int G, cudaStream_t st) {
+    // (the pool's release threshold is set on a device's first call, here and
+    // not only on the pooled branch: that branch is the one stream captures
+    // take, and setting a pool attribute inside a capture invalidates it)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) keep_pool_memory_fast();
+    cudaGetLastError();
+    if (owned(G, st)) return cudaSuccess;
+    cudaError_t e = cudaMallocAsync(&base, part_bytes(G) + flag_bytes(G), st);
+    if (e != cudaSuccess) return e;
+    point(base, G);
+    return cudaMemsetAsync(sk.flags, 0, flag_bytes(G), st);
   }
   void release(cudaStream_t st) {
     if (base) cudaFreeAsync(base, st);
@@ -1174,7 +1343,7 @@ struct SkWorkspace {
 // Stream-K launch over every SM (see the kernel's segment comment) of the
 // BM x BN units from unit0 on (unit numbering of the unit-mode kernel with
 // tile0 = 0).
-template <int VEC, int BM, int BN, int BK>
+template <int VEC, int BM, int BN, int BK, bool SUM = false>
 cudaError_t launch_streamk(const Epilogue &ep, int M, int N, int K, const double *A, int64_t lda, const double *B,
                            int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, long long unit0,
                            int after_main, cudaStream_t st, StreamK sk) {
@@ -1184,8 +1353,8 @@ cudaError_t launch_streamk(const Epilogue &ep, int M, int N, int K, const double
   sk.dp_tiles = 0;
   sk.tile0 = unit0;
   sk.iters = ((long long)tiles_m * tiles_n * PER_TILE - unit0) * KT;
-  return launch_one<VEC, BM, BN, BK, true>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
-                                           after_main, st, sk);
+  return launch_one<VEC, BM, BN, BK, true, SUM>(ep, (unsigned)G, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                                after_main, st, sk);
 }
 
 // stream-K over units of `split` per tile (1 = full tiles), from unit0 on
@@ -1213,6 +1382,21 @@ cudaError_t launch_streamk_split(const Epilogue &ep, int split, int M, int N, in
 }
 
 std::atomic<int> g_max_ctas{0};  // my_dgemm_set_max_ctas: 0 = every SM
+
+// The K-split plan is opt-in: MY_DGEMM_FORCE_KSPLIT per call, or
+// MY_DGEMM_KSPLIT=1 in the environment lets the heuristic cost it against the
+// plan-invariant plans (off by default: measured, it does not beat them --
+// 1024^3 77.7 vs 77.3 us, 1408^3 170.0 vs 172.4, 896^3 60.1 vs 52.4,
+// profiles/r02/ksplit_r02c.log -- because writing, re-reading and adding a
+// 128 KB accumulator block costs each CTA ~2 us per step, which eats what the
+// even split gains, profiles/r02/ksplit_timeline_r02b.log).
+bool ksplit_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("MY_DGEMM_KSPLIT");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
 
 // Round re-alignment of long-K whole-tile launches (MY_DGEMM_ROUND_SYNC=R,
 // default MYD_ROUND_SYNC: every R rounds; 0 = off; only K >= 16384, where a
@@ -1297,6 +1481,11 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
   using namespace fast;
+  // force_split < 0: the heuristic restricted to plan-invariant plans (no
+  // K-split); 48: the K-split plan when the shape allows it (else as < 0)
+  const bool force_ksplit = force_split == 48;
+  const bool allow_ksplit = force_split == 0 && ksplit_enabled();
+  if (force_split < 0 || force_ksplit) force_split = 0;
   const int tiles_m = (M + TILE_M - 1) / TILE_M, tiles_n = (N + TILE_N - 1) / TILE_N;
   const long long tiles = (long long)tiles_m * tiles_n;
   if (tiles > 0x7fffffffLL / 8) return cudaErrorInvalidConfiguration;
@@ -1310,8 +1499,23 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   auto per_tile = [](int s) { return s == 16 ? 8 : s; };
   int sk_split = force_split >= 32 ? (force_split == 32 ? 1 : force_split - 32) : 1;  // stream-K unit shape
   bool streamk = force_split >= 32 && force_split < 64 && tiles * sk_split >= G;
+  // K-split (sum) plan over full tiles, tiles < G (the kernel's segment
+  // comment; opt-in, see ksplit_enabled): pieces of a tile's K range on
+  // several SMs, partial sums added by the tile's owner.  Needs 16-byte
+  // staging (so the slab depth, hence the cut points, depend on K alone) and
+  // the whole device (the cut depends on the CTA count).  Cost: ceil(T KT / G)
+  // slabs per CTA at the stream-K slab rate, the fixed ramp with the piece
+  // boundary, and the owner's fix-up of G / T - 1 partials
+  // (tools/ksplit_probe.py, profiles/r02/ksplit_r02c.log).
+  const int ks_bk = full_bk<2>(K);
+  const long long ks_KT = (K + ks_bk - 1) / ks_bk;
+  const bool ks_ok = vec2 && tiles < G && tiles * ks_KT >= 2 * G && tiles * ks_KT < (1LL << 30) &&
+                     g_max_ctas.load(std::memory_order_relaxed) == 0;
+  bool ksplit = force_ksplit && ks_ok;
   double plan_best = 1e300;  // the heuristic's cost of its persistent-kernel plan (us)
-  if (force_split >= 64) {
+  if (ksplit) {
+    q = tiles;
+  } else if (force_split >= 64) {
     q = tiles;  // small-block kernel, below
   } else if (force_split >= 32) {
     q = tiles;  // (fewer units than SMs: plain full tiles instead)
@@ -1435,6 +1639,16 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         }
       }
     }
+    if (allow_ksplit && ks_ok) {
+      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)ks_KT;
+      const double cost = (double)((tiles * ks_KT + G - 1) / G) * slab_us + 3 * unit_b(1) + 8.0 +
+                          MYD_KSPLIT_FIXUP_US * ((double)G / (double)tiles);
+      if (cost < best - 1e-9) {
+        best = cost;
+        ksplit = true;
+        streamk = false;
+      }
+    }
     plan_best = best;
   }
   // Small-block kernel (dgemm_small.cu): below a few waves of units, CTAs
@@ -1451,7 +1665,7 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         if (c < sbest) sbest = c, small_v = v;
       }
     }
-  } else if (force_split == 0 && tiles <= 2 * G && g_max_ctas.load(std::memory_order_relaxed) == 0) {
+  } else if (force_split == 0 && !force_ksplit && tiles <= 2 * G && g_max_ctas.load(std::memory_order_relaxed) == 0) {
     // (not under an SM cap: its grid is the block count, not a persistent
     // grid the cap could bound; results do not depend on the choice)
     double sbest = plan_best;
@@ -1467,9 +1681,21 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   if (trace)
     fprintf(stderr,
             "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d q=%lld raster=%dx%d edge=%d small=%d\n",
-            M, N, K, (long long)tiles_m, tiles_n, small_v ? "small" : (streamk ? "stream-K" : "units"), split, sk_split, q,
-            raster_m, raster_n, edge, small_v);
+            M, N, K, (long long)tiles_m, tiles_n,
+            small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, q, raster_m,
+            raster_n, edge, small_v);
   if (small_v > 0) return launch_dgemm_small(small_v, M, N, K, A, lda, B, ldb, C, ldc, stream, ep, vec2);
+  if (ksplit) {
+    SkWorkspace ws;
+    cudaError_t e = ws.alloc((int)G, stream);
+    if (e == cudaSuccess)
+      e = ks_bk == 32 ? launch_streamk<2, 128, 128, 32, true>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                                              stream, ws.sk)
+                      : launch_streamk<2, 128, 128, 16, true>(ep, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, 0, 0,
+                                                              stream, ws.sk);
+    ws.release(stream);
+    return e;
+  }
   if (streamk) {
     SkWorkspace ws;
     cudaError_t e = ws.alloc((int)G, stream);
@@ -1578,6 +1804,15 @@ extern "C" __attribute__((visibility("default"))) void my_dgemm_timeline(unsigne
   if (reset) {
     unsigned long long z[32] = {~0ull};
     cudaMemcpyToSymbol(myd::g_tl, z, sizeof z);
+  }
+}
+#endif
+#ifdef MYD_KS_TIMELINE
+extern "C" __attribute__((visibility("default"))) void my_dgemm_ks_timeline(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, myd::g_kst, sizeof(unsigned long long) * 160 * 16);
+  if (reset) {
+    static unsigned long long z[160 * 16];
+    cudaMemcpyToSymbol(myd::g_kst, z, sizeof z);
   }
 }
 #endif

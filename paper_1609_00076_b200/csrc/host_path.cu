@@ -93,6 +93,8 @@ int host_path(int m, int n, int k, const double *A, int lda, const double *B, in
   const double flops = 2.0 * m * (double)n * k;
   // (the column panels and k-chunks are bitwise the one call only on the tiled path)
   const bool pipelined = flops > 4e9 && n >= 1024 && path_kind(m, n, flags) == MY_DGEMM_PATH_TILED;
+  // (its panels and k-chunks must each keep the one call's arithmetic: plan-invariant plans only)
+  if (pipelined) flags |= MY_DGEMM_PLAN_INVARIANT;
   // Column group 0 is computed in k-chunks while A uploads; it only needs to
   // be wide enough that each chunk's GEMM outlasts the next chunk's upload
   // (flop per uploaded byte 2 m nc0 / (8 (m + nc0)) against 36.7 TF over

@@ -141,6 +141,7 @@ def check_conformal(a, b, c) -> tuple[int, int, int]:
 _STRIPS_FLAGS = {0: 0, 1: _capi.FORCE_TILES, 2: _capi.FORCE_STRIPS2, 4: _capi.FORCE_STRIPS4, 8: _capi.FORCE_UNITS8,
                  16: _capi.FORCE_ROWS16, 32: _capi.FORCE_STREAMK, 34: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS2,
                  36: _capi.FORCE_STREAMK | _capi.FORCE_STRIPS4, 40: _capi.FORCE_STREAMK | _capi.FORCE_UNITS8,
+                 48: _capi.FORCE_KSPLIT, -1: _capi.PLAN_INVARIANT,
                  **{64 + v: _capi.FORCE_SMALL | _capi.SMALL_VARIANT(v) for v in range(16)}}
 
 
@@ -254,8 +255,11 @@ def dgemm_device(m, n, k, a_ptr: int, lda: int, b_ptr: int, ldb: int, c_ptr: int
     128x32 / 64x32 / 16x128 units, 32 / 34 / 36 / 40 the stream-K schedule
     over full tiles / those units, 64 + v the small-block kernel's variant v
     (1..10; 64: the planner's pick); `path` forces a kernel family
-    (_capi.PATH_*, what sharded drivers pass to every shard).  Every plan
-    gives bitwise the same C."""
+    (_capi.PATH_*, what sharded drivers pass to every shard).  Every one of
+    these plans gives bitwise the same C.  48 is the opt-in K-split plan
+    (MY_DGEMM_FORCE_KSPLIT: deterministic and within the tolerance, but not
+    that same chain), -1 the heuristic kept to the plan-invariant plans
+    (MY_DGEMM_PLAN_INVARIANT; the default unless MY_DGEMM_KSPLIT=1)."""
     lib = _capi._lib or _capi.load()
     if exact or force_tiled or force_vec1 or strips or path is not None:
         flags = _flags(exact, force_tiled, force_vec1, strips, path) | _capi.DEVICE_PTRS
@@ -388,16 +392,18 @@ def kernel_launches() -> int:
 
 
 def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A, lda: int, B, ldb: int,
-          beta: float, C, ldc: int, exact: bool = False, stream: int | None = None, epilogue: bool = False):
+          beta: float, C, ldc: int, exact: bool = False, stream: int | None = None, epilogue: bool = False,
+          plan: int = 0):
     """BLAS dgemm: C := alpha op(A) op(B) + beta C.
 
     Host numpy buffers (synchronous) or torch CUDA tensors (asynchronous on
     `stream`, default torch's current stream).  Argument errors raise
     ValueError naming the BLAS parameter.  `epilogue` (tests) forces alpha /
-    beta into the kernel epilogue instead of the reference-BLAS order.
+    beta into the kernel epilogue instead of the reference-BLAS order; `plan`
+    pins the launch plan of the tiled kernel (dgemm_device's `strips`).
     """
     lib = _capi.load()
-    flags = _flags(exact) | (_capi.BLAS_EPILOGUE if epilogue else 0)
+    flags = _flags(exact, strips=plan) | (_capi.BLAS_EPILOGUE if epilogue else 0)
     dev = _is_device(C)
     if dev:
         if stream is None:

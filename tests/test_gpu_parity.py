@@ -305,6 +305,54 @@ def test_strip_plans_bitwise_equal(torch_cuda, m, n, k, lda, ldb, ldc):
         assert np.all(host.reshape(n, ldc)[:, m:] == -777.25)
 
 
+@pytest.mark.parametrize("m,n,k,lda,ldb,ldc", [
+    (1024, 1024, 1024, 1024, 1024, 1024),   # 64 tiles, 32 slabs of 32: tiles cut into 2-3 pieces
+    (1280, 1152, 1100, 1280, 1100, 1282),   # 32-deep slabs with a ragged last one
+    (512, 512, 512, 512, 512, 512),         # 16 tiles, 16-deep slabs: ~9 pieces per tile
+    (1000, 1100, 777, 1002, 778, 1000),     # ragged tiles, ragged last slab
+    (768, 640, 96, 768, 96, 768),           # short K: fewer slabs than 2 per CTA -> not applicable
+    (777, 1029, 201, 781, 205, 780),        # odd lda / ldb: staged from even-ld scratch copies
+    (300, 200, 100, 301, 101, 300),         # odd lda / ldb, small: 8-byte staging -> not applicable
+])
+def test_k_split_plan_is_opt_in_deterministic_and_within_the_bound(torch_cuda, m, n, k, lda, ldb, ldc):
+    """The K-split plan (plan 48, MY_DGEMM_FORCE_KSPLIT): a tile's K range in
+    pieces on several SMs, partial sums added by the tile's owner in CTA
+    order.  It is the one plan that is not the single ascending chain, so it
+    is opt-in: the default call and MY_DGEMM_PLAN_INVARIANT stay bitwise the
+    other plans.  Forced, it is run-to-run bitwise deterministic, within the
+    headline bound of the exact kernel, keeps the padding, and falls back to
+    the plan-invariant heuristic where the shape does not allow it."""
+    a, b, c, _ = dev_operands(torch_cuda, m, n, k, lda, ldb, ldc, canary=-777.25)
+    outs = {}
+    for strips in (0, -1, 2, 48, 48):
+        cc = c.clone()
+        run_dev(torch_cuda, m, n, k, a, lda, b, ldb, cc, ldc, strips=strips)
+        outs.setdefault(strips, []).append(cc)
+    assert torch_cuda.equal(outs[0][0], outs[-1][0]) and torch_cuda.equal(outs[0][0], outs[2][0])
+    assert torch_cuda.equal(outs[48][0], outs[48][1])
+    ce = c.clone()
+    run_dev(torch_cuda, m, n, k, a, lda, b, ldb, ce, ldc, exact=True)
+    bound = device_bound(torch_cuda, m, n, k, a, lda, b, ldb, c, ldc)
+    check_dev(torch_cuda, m, n, k, outs[48][0], ce, ldc, bound)
+    tiles = -(-m // 128) * -(-n // 128)
+    vec2 = (lda % 2 == 0 and ldb % 2 == 0) or m * n * k >= 1 << 24 or k >= 512  # (odd lds: even-ld scratch copies)
+    applicable = vec2 and tiles < 148 and tiles * -(-k // (32 if k >= 1024 else 16)) >= 2 * 148
+    if not applicable:
+        assert torch_cuda.equal(outs[48][0], outs[0][0])
+    host = outs[48][0].cpu().numpy()
+    if ldc > m:
+        assert np.all(host.reshape(n, ldc)[:, m:] == -777.25)
+    # the BLAS epilogue on the K-split plan: alpha (A B) + beta C applied by the owner after the fix-up
+    if applicable:
+        cb = c.clone()
+        engine.dgemm("N", "N", m, n, k, -0.5, a, lda, b, ldb, 0.25, cb, ldc, epilogue=True, plan=48)
+        torch_cuda.cuda.synchronize()
+        want = 0.25 * c.view(n, ldc)[:, :m] - 0.5 * (ce.view(n, ldc)[:, :m] - c.view(n, ldc)[:, :m])
+        assert float((cb.view(n, ldc)[:, :m] - want).abs().max()) <= 2 * bound
+        if ldc > m:
+            assert bool((cb.view(n, ldc)[:, m:] == -777.25).all())
+
+
 SMALL_PLANS = tuple(range(64, 75))  # the small-block kernel: planner's pick, then variants 1..10
 
 
