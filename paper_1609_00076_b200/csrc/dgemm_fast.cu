@@ -1499,6 +1499,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   auto per_tile = [](int s) { return s == 16 ? 8 : s; };
   int sk_split = force_split >= 32 ? (force_split == 32 ? 1 : force_split - 32) : 1;  // stream-K unit shape
   bool streamk = force_split >= 32 && force_split < 64 && tiles * sk_split >= G;
+  // whole-tile rounds ahead of a full-tile stream-K phase (forced plan 32: all
+  // but the last one to two waves; MY_DGEMM_SK_DP_ROUNDS overrides, for probes)
+  long long sk_dp_rounds = std::max(0LL, tiles / G - 1);
   // K-split (sum) plan over full tiles, tiles < G (the kernel's segment
   // comment; opt-in, see ksplit_enabled): pieces of a tile's K range on
   // several SMs, partial sums added by the tile's owner.  Needs 16-byte
@@ -1587,35 +1590,50 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // Below one wave of tiles: stream-K over units (>= one unit per CTA, so a
     // unit is cut at most once), when the problem has no ragged edge (empty
     // units would be scheduled, not skipped).
-    if (tiles < G && M % TILE_M == 0 && N % TILE_N == 0)
-      for (int s : {2, 4, 8}) {
-        const long long units_s = tiles * s;
-        const int bk = s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : default_bk<64, 32>());
-        const long long KT = (K + bk - 1) / bk;
-        if (units_s < G || units_s * KT >= (1LL << 30)) continue;
-        // stream-K phase slabs run ~2 % slower than whole units (~15 % for 64x32 units)
-        const double slab_us = (s == 8 ? 1.15 : 1.02) * (unit_us(s) - unit_b(s)) / (double)KT;
-        const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + 3 * unit_b(s) + 2.0;
-        if (cost < best - 1e-9) {
-          best = cost;
-          streamk = true;
-          sk_split = s;
-        }
-      }
-    // Data-parallel rounds for all but the last (one to two waves of tiles).
-    if (tiles >= G && tiles % G != 0 && (G + tiles % G) * (long long)(K / 16 + 1) < (1LL << 30)) {
-      const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
-      const long long KT = (K + bk - 1) / bk, sk_tiles = G + tiles % G;
-      // the stream-K phase runs ~2 % slower per slab than whole tiles, and
-      // its launch, a PDL tail of the whole-tile rounds, costs ~5 us
-      // (tools/perf_probe.py --strips=32, profiles/plan_probe_sk_r01.log)
-      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)KT;
-      const double cost = (double)(tiles / G - 1) * unit_us(1) + (tiles >= 2 * G ? 5.0 : 0.0) +
-                          (double)((sk_tiles * KT + G - 1) / G) * slab_us + 3 * unit_b(1) + 2.0;
+    // Round 2 (workspace owned by the stream, no per-call memset): refitted on
+    // 640..1536^3 (tools/midsize_plans.py, profiles/r02/midsize_plans_r02a.log;
+    // residuals < 0.6 us): a stream-K slab of 128x64 / 128x32 / 64x32 units
+    // costs 1.037 / 1.058 / 1.086 of the whole-unit slab, the call 12.0 / 10.3 /
+    // 9.9 us on top.  The same schedule is also costed above one wave of tiles
+    // (every unit of the problem in the stream-K phase, ragged edges included:
+    // their empty units are scheduled and cost their slabs, as modelled).
+    for (int s : {2, 4, 8}) {
+      const long long units_s = tiles * s;
+      const int bk = s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : default_bk<64, 32>());
+      const long long KT = (K + bk - 1) / bk;
+      if (units_s < G || units_s * KT >= (1LL << 30)) continue;
+      if (tiles < G && (M % TILE_M != 0 || N % TILE_N != 0)) continue;  // (the edge plans cover these)
+      const double f = s == 2 ? 1.037 : (s == 4 ? 1.058 : 1.086), fixed = s == 2 ? 12.0 : (s == 4 ? 10.3 : 9.9);
+      const double slab_us = f * (unit_us(s) - unit_b(s)) / (double)KT;
+      const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + fixed;
       if (cost < best - 1e-9) {
         best = cost;
         streamk = true;
-        sk_split = 1;
+        sk_split = s;
+      }
+    }
+    // Data-parallel rounds for all but the last (one to two waves of tiles).
+    // Either every tile in the stream-K phase (no whole-tile rounds), or all
+    // but the last one to two waves as whole tiles: the stream-K phase runs
+    // ~2 % slower per slab than whole tiles, but following a whole-tile launch
+    // costs it ~20 us (refit on 1664..3072^3, profiles/r02/midsize_plans_r02a.log:
+    // the model with the round-1 5 us was 20 us under wherever there were
+    // whole-tile rounds and 5.5 us under where there were none).
+    if (tiles >= G && tiles % G != 0) {
+      const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
+      const long long KT = (K + bk - 1) / bk;
+      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)KT;
+      for (long long d : {0LL, tiles / G - 1}) {
+        const long long sk_tiles = tiles - d * G;
+        if (sk_tiles * KT >= (1LL << 30)) continue;
+        const double cost = (double)d * unit_us(1) + (d > 0 ? 20.0 : 0.0) +
+                            (double)((sk_tiles * KT + G - 1) / G) * slab_us + 16.0;
+        if (cost < best - 1e-9) {
+          best = cost;
+          streamk = true;
+          sk_split = 1;
+          sk_dp_rounds = d;
+        }
       }
     }
     const int rem_m = M % TILE_M;
@@ -1680,10 +1698,11 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   }();
   if (trace)
     fprintf(stderr,
-            "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d q=%lld raster=%dx%d edge=%d small=%d\n",
+            "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d sk_dp_rounds=%lld q=%lld raster=%dx%d "
+            "edge=%d small=%d\n",
             M, N, K, (long long)tiles_m, tiles_n,
-            small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, q, raster_m,
-            raster_n, edge, small_v);
+            small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, sk_dp_rounds, q,
+            raster_m, raster_n, edge, small_v);
   if (small_v > 0) return launch_dgemm_small(small_v, M, N, K, A, lda, B, ldb, C, ldc, stream, ep, vec2);
   if (ksplit) {
     SkWorkspace ws;
@@ -1713,7 +1732,13 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     }
     // whole-tile rounds for all but the last one-to-two waves in the unit-mode
     // kernel, then the stream-K phase as a tail launch (its own tiles only)
-    const long long dp_tiles = (tiles / G - 1) * G;
+    static const long long dp_env = [] {
+      const char *v = getenv("MY_DGEMM_SK_DP_ROUNDS");
+      return v && *v ? atoll(v) : -1LL;
+    }();
+    if (dp_env >= 0) sk_dp_rounds = std::min(dp_env, std::max(0LL, tiles / G - 1));
+    if ((tiles - sk_dp_rounds * G) * (long long)(K / 16 + 1) >= (1LL << 30)) sk_dp_rounds = std::max(0LL, tiles / G - 1);
+    const long long dp_tiles = sk_dp_rounds * G;
     RoundSync rsync;
     if (dp_tiles > 0) {
       e = rsync.setup(dp_tiles, G, M % TILE_M != 0 || N % TILE_N != 0, K, stream);
