@@ -1605,7 +1605,9 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       if (tiles < G && (M % TILE_M != 0 || N % TILE_N != 0)) continue;  // (the edge plans cover these)
       const double f = s == 2 ? 1.037 : (s == 4 ? 1.058 : 1.086), fixed = s == 2 ? 12.0 : (s == 4 ? 10.3 : 9.9);
       const double slab_us = f * (unit_us(s) - unit_b(s)) / (double)KT;
-      const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + fixed;
+      // (the fit covers 1.3 - 2.9 units per CTA; each further unit boundary ~3 us)
+      const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + fixed +
+                          3.0 * std::max(0.0, (double)units_s / (double)G - 2.0);
       if (cost < best - 1e-9) {
         best = cost;
         streamk = true;
@@ -1618,7 +1620,10 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // ~2 % slower per slab than whole tiles, but following a whole-tile launch
     // costs it ~20 us (refit on 1664..3072^3, profiles/r02/midsize_plans_r02a.log:
     // the model with the round-1 5 us was 20 us under wherever there were
-    // whole-tile rounds and 5.5 us under where there were none).
+    // whole-tile rounds and 5.5 us under where there were none).  A tile
+    // boundary inside the phase costs ~3.2 us (no split boundary there), which
+    // is what keeps short-K problems on whole-tile rounds (cfg4 with every
+    // tile in the phase: 4.05 ms vs 3.93 ms).
     if (tiles >= G && tiles % G != 0) {
       const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
       const long long KT = (K + bk - 1) / bk;
@@ -1627,7 +1632,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         const long long sk_tiles = tiles - d * G;
         if (sk_tiles * KT >= (1LL << 30)) continue;
         const double cost = (double)d * unit_us(1) + (d > 0 ? 20.0 : 0.0) +
-                            (double)((sk_tiles * KT + G - 1) / G) * slab_us + 16.0;
+                            (double)((sk_tiles * KT + G - 1) / G) * slab_us + 12.0 +
+                            3.2 * (double)sk_tiles / (double)G;
         if (cost < best - 1e-9) {
           best = cost;
           streamk = true;
