@@ -136,6 +136,13 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_KSPLIT_FIXUP_US
 #define MYD_KSPLIT_FIXUP_US 2.5  // K-split plan: owner's fix-up cost per piece of a tile (us, planner model)
 #endif
+#ifndef MYD_EDGE_BULK
+#define MYD_EDGE_BULK 1  // ragged problems of up to MYD_EDGE_BULK_WAVES waves of tiles run the EDGE instantiations:
+                         // partial units staged by bulk copies of their valid part (0: zero-filling LDGSTS everywhere)
+#endif
+#ifndef MYD_EDGE_BULK_WAVES
+#define MYD_EDGE_BULK_WAVES 4
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -216,7 +223,8 @@ constexpr int PROBE_STEP = 1;  // k-step at which the next slab's barrier is pro
 // full[s] completes when slab s has landed (bulk-copy transaction bytes or
 // LDGSTS completions); empty[s] when all 8 consumers have their fragments of
 // slab s in registers.  No CTA-wide barrier in the main loop.
-template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false>
+template <int VEC, int BM, int BN, int BKT, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false,
+          bool EDGE = false>
 __global__ void __launch_bounds__(fast::THREADS, 1)
     dgemm_fast_kernel(int M, int N, int K, const double *__restrict__ A, int64_t lda, const double *__restrict__ B,
                       int64_t ldb, double *__restrict__ C, int64_t ldc, int tiles_m, int tiles_n, int tile0, int edge,
@@ -591,6 +599,51 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
           if (blockIdx.x == 0 && pw == 0 && lane == 0 && first_seg && kt == sg.kb) g_tl[7] = gtimer();
 #endif
           continue;
+        }
+        if constexpr (BULK_UNIT && VEC == 2 && EDGE) {
+          // Partial units (the ragged last tile row / column) on a full K slab:
+          // bulk copies of the valid part only -- each k-row of A over the
+          // unit's valid rows (an even count; the last row of an odd one by an
+          // 8-byte cp.async), each valid column of B.  Rows and columns past
+          // M and N keep whatever the slot held: they only ever reach
+          // accumulators that are never stored (an element of C depends on
+          // its own row of A and column of B alone), so they need no zero
+          // fill -- unlike a ragged last K slab, which stays on the
+          // zero-filling LDGSTS path below.  Bounds-checked LDGSTS made a
+          // partial unit 1.3 - 1.7x as long as a whole one
+          // (profiles/r02/planner_regret_r02b.log).  Its own instantiation
+          // (EDGE, launch_one): with this code in every kernel the whole-tile
+          // kernel lost 8 % at cfg4 and 0.3 % at 8192^3 on problems that have
+          // no partial unit at all (profiles/r02/ab_libs_r02d.log).
+          if (kbase + BK <= K) {
+            constexpr int A_ROWS = BK / PRODUCER_WARPS;
+            const int vcols = max(0, min(BN, N - n0));
+            const int vrows = vcols > 0 ? max(0, min(BM, M - m0)) : 0;  // (an empty unit stages nothing)
+            const int ev = vrows & ~1;
+            const bool a_mine = lane < A_ROWS && ev > 0;
+            const bool b_mine = vrows > 0 && lane < RW && pw * RW + lane < vcols;
+            if (vrows & 1) {
+              if (lane < A_ROWS) {
+                const int kk = pw * A_ROWS + lane;
+                cp_async<8>(as + kk * AP + ev, A + (int64_t)(kbase + kk) * lda + m0 + ev, 8);
+              }
+              cp_async_mbar_arrive_inc(&full_bar[slot]);
+              __syncwarp();
+            }
+            const uint32_t bytes = (uint32_t)__popc(__ballot_sync(0xffffffffu, a_mine)) * ev * 8 +
+                                   (uint32_t)__popc(__ballot_sync(0xffffffffu, b_mine)) * BK * 8;
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[slot], bytes);
+            __syncwarp();
+            if (a_mine) {
+              const int kk = pw * A_ROWS + lane;
+              bulk_g2s(as + kk * AP, A + (int64_t)(kbase + kk) * lda + m0, ev * 8, &full_bar[slot]);
+            }
+            if (b_mine) {
+              const int nn = pw * RW + lane;
+              bulk_g2s(bs + nn * BP, B + (int64_t)(n0 + nn) * ldb + kbase, BK * 8, &full_bar[slot]);
+            }
+            continue;
+          }
         }
         // A slab [BK][BM], m contiguous: a warp instruction covers 32*VEC
         // consecutive m of one k-row (coalesced, conflict-free at pitch AP).
@@ -1130,7 +1183,8 @@ bool pdl_enabled() {
   return on;
 }
 
-template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false>
+template <int VEC, int BM, int BN, int BK, bool SKM, bool CGT, bool RK, bool RS = false, bool SUM = false,
+          bool EDGE = false>
 cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int K, const double *A, int64_t lda,
                           const double *B, int64_t ldb, double *C, int64_t ldc, int tiles_m, int tiles_n, int tile0,
                           int edge, int after_main, cudaStream_t st, const StreamK &sk) {
@@ -1146,7 +1200,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
       cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)MYD_L2_PERSIST_MB << 20);
       cudaGetLastError();
     }
-    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM>,
+    cudaError_t e = cudaFuncSetAttribute(dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM, EDGE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<BM, BN, BK>::BYTES);
     if (e != cudaSuccess) return e;
     attr_done.fetch_or(bit, std::memory_order_release);
@@ -1165,7 +1219,7 @@ cudaError_t launch_kernel(const Epilogue &ep, unsigned units, int M, int N, int 
   attr[1].val.cooperative = 1;
   cfg.attrs = pdl_enabled() ? attr : attr + 1;
   cfg.numAttrs = (pdl_enabled() ? 1 : 0) + (RS ? 1 : 0);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM>, M, N, K, A, lda, B, ldb,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, dgemm_fast_kernel<VEC, BM, BN, BK, SKM, CGT, RK, RS, SUM, EDGE>, M, N, K, A, lda, B, ldb,
                                      C, ldc, tiles_m, tiles_n, tile0, edge, (int)units, after_main, sk, ep);
   count_launch();
   if (e != cudaSuccess) return e;
@@ -1187,9 +1241,22 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   // each element sees (hence C, bitwise, even the sign of a zero) does not
   // depend on the plan or on which kernel a shard's tile lands in.
   const bool rk = MYD_SKIP_ZERO_KSTEPS && K % BK != 0 && BK - K % BK >= 4;
+  // partial units worth their own instantiation (see the EDGE staging path)
+  [[maybe_unused]] const bool edge_bulk =
+      (M % BM != 0 || N % BN != 0) &&
+      (long long)((M + fast::TILE_M - 1) / fast::TILE_M) * ((N + fast::TILE_N - 1) / fast::TILE_N) <=
+          (long long)MYD_EDGE_BULK_WAVES * sm_count();
 #define MYD_LAUNCH(CGT_, RK_)                                                                                   \
-  return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_, false, SUM>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, \
-                                                                    tiles_n, tile0, edge, after_main, st, sk)
+  do {                                                                                                            \
+    if constexpr (VEC == 2 && BM != 16 && MYD_EDGE_BULK) {                                                        \
+      if (edge_bulk)                                                                                              \
+        return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_, false, SUM, true>(                                  \
+            ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st, sk);       \
+    }                                                                                                             \
+    return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_, false, SUM>(ep, units, M, N, K, A, lda, B, ldb, C, ldc, \
+                                                                      tiles_m, tiles_n, tile0, edge, after_main,  \
+                                                                      st, sk);                                    \
+  } while (0)
   if constexpr (VEC == 2 && BM == 128 && BN == 128) {
     if (c_aligned) {
       if constexpr (BK == 32 && !SKM) {
@@ -1526,25 +1593,60 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     split = force_split >= 16 ? 16 : (force_split >= 8 ? 8 : (force_split >= 4 ? 4 : 2));  // every tile as units
     q = 0;
   } else if (force_split == 0) {
-    // one unit of 1/s tile, depth K, on one SM: ideal / e_s + b_s microseconds
-    // (fitted: tools/plan_probe.py, profiles/plan_probe_r01b.log; b_8 refitted
-    // on whole-call timings of 256-4096^3, tools/midsize_plans.py,
-    // profiles/midsize_plans_r01.log, where 4 us instead of 2 stops 64x32
-    // units winning at 768-1280^3 by a model margin they do not have; 16x128
-    // units, LDGSTS-staged, refitted on tools/rows16_probe.py and short-K
-    // ragged rows (tools/plans_for.py): e 0.74, b 2)
-    auto unit_b = [](int s) { return s == 1 ? 2.8 : (s == 2 ? 7.2 : (s == 4 ? 4.4 : (s == 16 ? 2.0 : 4.0))); };
-    auto unit_us = [&](int s) {
-      const double ideal = 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3;
-      const double e = s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : (s == 16 ? 0.740 : 0.977)));
-      return ideal / e + unit_b(s);
+    // A launch of r rounds of 1/s-tile units at depth K costs launch_us(s) +
+    // r * round_us(s) microseconds: refitted in round 2 on whole calls of
+    // exactly r * 148 units, r = 1..8, K = 64..4096 (tools/unit_model_probe.py,
+    // profiles/r02/unit_model_r02a.log).  The round-1 model (ideal / e_s + b_s
+    // per round, b = 2.8 / 7.2 / 4.4 / 4.0 us, no per-launch term) charged the
+    // narrow units' launch ramp to every round -- several rounds of 128x64
+    // units at K = 128 looked 40 % dearer than they are (5376 x 1536 x 128:
+    // full tiles 93.8 us, the 128x64 units it rejected 78.3 us,
+    // profiles/r02/planner_regret_r02a.log) -- and their DMMA rate at long K
+    // 3 % better than it is.  16x128 units (LDGSTS-staged) keep the round-1
+    // fit on tools/rows16_probe.py and short-K ragged rows: e 0.74, b 2.
+    auto ideal_us = [&](int s) { return 2.0 * TILE_M * TILE_N / per_tile(s) * K / 251.5e3; };
+    auto round_us = [&](int s) -> double {
+      // a ragged last K slab is staged by zero-filling LDGSTS: ~1.7 us per unit
+      // (2582 x 1906 x 144 as 128x32 units, 32-deep slabs: 73.7 us against 58.1 modelled)
+      const int bk = s == 1 ? (vec2 ? full_bk<2>(K) : full_bk<1>(K))
+                            : (s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : (s == 16 ? MYD_ROWS16_BK : default_bk<64, 32>())));
+      const double ideal = ideal_us(s) + (K % bk != 0 ? 1.7 : 0.0);
+      switch (s) {
+        case 1: return ideal / 0.986 + 2.8 + (K < 128 ? 0.05 * (128 - K) : 0.0);
+        case 2: return ideal / 0.953 + 1.26;
+        case 4: return ideal / 0.957 + 0.86;
+        case 16: return ideal / 0.740 + 2.0;
+        // (+1 us per round over the fit on whole, balanced rounds: on real shapes 64x32 units
+        // come out ~5 % behind it, 1000 x 1100 x 1200: 96.5 us against 91.4 modelled)
+        default: return ideal / 0.945 + 1.48 + std::max(0.0, 1.7 - K / 300.0);
+      }
+    };
+    auto launch_us = [&](int s, double r = 2.0) -> double {
+      switch (s) {
+        case 1: return 11.5;
+        case 2: return 7.2;
+        case 4: return 6.3;
+        case 16: return 0.0;
+        // (a single round of 64x32 units ends ~3 us sooner than the fit on 2..8 rounds says: 512^3 13.4 us)
+        default: return std::min(r <= 1.0 ? 4.0 : 6.8, 1.0 + K / 40.0);
+      }
+    };
+    // (the stream-K fits below are relative to the round-1 unit work, ideal / e_s)
+    auto sk_work_us = [&](int s) {
+      return ideal_us(s) / (s == 1 ? 0.990 : (s == 2 ? 0.984 : (s == 4 ? 0.983 : 0.977)));
     };
     auto rounds = [&](long long units) { return (double)((units + G - 1) / G); };
-    constexpr double SECOND_LAUNCH_US = 15.0;
-    double best = rounds(tiles) * unit_us(1);  // full tiles only
+    constexpr double TAIL_LAUNCH_US = 16.0;  // a second (PDL tail) launch after whole-tile rounds
+    // (Partial units of a ragged M or N cost what whole ones do since their
+    // valid part is staged by bulk copies; with zero-filling LDGSTS they ran
+    // 1.3 - 1.7x as long and a one- or two-round call could not hide the one
+    // some CTA always got: 506 x 1188 x 1616 as 64x32 units 113 us against 92
+    // modelled, profiles/r02/planner_regret_r02b.log.)
+    const bool ragged_mn = M % TILE_M != 0 || N % TILE_N != 0;
+    double best = launch_us(1) + rounds(tiles) * round_us(1);  // full tiles only
     q = tiles;  // (split == 1: one launch of every tile)
     for (int s : {2, 4, 8}) {
-      const double all = rounds(tiles * s) * unit_us(s);
+      const double all = launch_us(s, rounds(tiles * s)) + rounds(tiles * s) * round_us(s);
       if (all < best - 1e-9) {
         best = all;
         split = s;
@@ -1552,7 +1654,7 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       }
       const long long q1 = tiles / G, r1 = tiles % G;
       if (q1 > 0 && r1 > 0) {
-        const double tail = q1 * unit_us(1) + rounds(r1 * s) * unit_us(s) + SECOND_LAUNCH_US;
+        const double tail = launch_us(1) + q1 * round_us(1) + rounds(r1 * s) * round_us(s) + TAIL_LAUNCH_US;
         if (tail < best - 1e-9) {
           best = tail;
           split = s;
@@ -1572,8 +1674,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         const int bn = s == 2 ? 64 : 32;
         const int ns = (rem_n + bn - 1) / bn;  // valid strips of the 128x64 / 128x32 / 64x32 units
         const long long nonempty = re * s + (long long)tiles_m * (s == 8 ? 2 : 1) * ns;
-        const double cost =
-            (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
+        const double cost = (qe > 0 ? launch_us(1) + qe * round_us(1) + TAIL_LAUNCH_US : launch_us(s, rounds(nonempty))) +
+                            rounds(nonempty) * round_us(s);
         if (cost < best - 1e-9) {
           best = cost;
           split = s;
@@ -1595,16 +1697,17 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // residuals < 0.6 us): a stream-K slab of 128x64 / 128x32 / 64x32 units
     // costs 1.037 / 1.058 / 1.086 of the whole-unit slab, the call 12.0 / 10.3 /
     // 9.9 us on top.  The same schedule is also costed above one wave of tiles
-    // (every unit of the problem in the stream-K phase, ragged edges included:
-    // their empty units are scheduled and cost their slabs, as modelled).
+    // and on ragged problems (every unit of the problem in the stream-K phase:
+    // empty units are scheduled and cost their slabs, as modelled; m and n of
+    // at least a tile, so most units are whole).
     for (int s : {2, 4, 8}) {
       const long long units_s = tiles * s;
       const int bk = s == 2 ? default_bk<128, 64>() : (s == 4 ? default_bk<128, 32>() : default_bk<64, 32>());
       const long long KT = (K + bk - 1) / bk;
       if (units_s < G || units_s * KT >= (1LL << 30)) continue;
-      if (tiles < G && (M % TILE_M != 0 || N % TILE_N != 0)) continue;  // (the edge plans cover these)
+      if (ragged_mn && (M < TILE_M || N < TILE_N)) continue;  // (narrower than a tile: the edge plans)
       const double f = s == 2 ? 1.037 : (s == 4 ? 1.058 : 1.086), fixed = s == 2 ? 12.0 : (s == 4 ? 10.3 : 9.9);
-      const double slab_us = f * (unit_us(s) - unit_b(s)) / (double)KT;
+      const double slab_us = f * sk_work_us(s) / (double)KT;
       // (the fit covers 1.3 - 2.9 units per CTA; each further unit boundary ~3 us)
       const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + fixed +
                           3.0 * std::max(0.0, (double)units_s / (double)G - 2.0);
@@ -1618,20 +1721,21 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     // Either every tile in the stream-K phase (no whole-tile rounds), or all
     // but the last one to two waves as whole tiles: the stream-K phase runs
     // ~2 % slower per slab than whole tiles, but following a whole-tile launch
-    // costs it ~20 us (refit on 1664..3072^3, profiles/r02/midsize_plans_r02a.log:
-    // the model with the round-1 5 us was 20 us under wherever there were
-    // whole-tile rounds and 5.5 us under where there were none).  A tile
+    // costs it ~17 us (the whole-tile launch's own 11.5 us and ~5 us of
+    // hand-over; refit on 1664..3072^3, profiles/r02/midsize_plans_r02a.log:
+    // the round-1 model was 20 us under wherever there were whole-tile rounds
+    // and 5.5 us under where there were none).  A tile
     // boundary inside the phase costs ~3.2 us (no split boundary there), which
     // is what keeps short-K problems on whole-tile rounds (cfg4 with every
     // tile in the phase: 4.05 ms vs 3.93 ms).
     if (tiles >= G && tiles % G != 0) {
       const int bk = vec2 ? full_bk<2>(K) : full_bk<1>(K);
       const long long KT = (K + bk - 1) / bk;
-      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)KT;
+      const double slab_us = 1.02 * sk_work_us(1) / (double)KT;
       for (long long d : {0LL, tiles / G - 1}) {
         const long long sk_tiles = tiles - d * G;
         if (sk_tiles * KT >= (1LL << 30)) continue;
-        const double cost = (double)d * unit_us(1) + (d > 0 ? 20.0 : 0.0) +
+        const double cost = (d > 0 ? launch_us(1) + (double)d * round_us(1) + 5.0 : 0.0) +
                             (double)((sk_tiles * KT + G - 1) / G) * slab_us + 12.0 +
                             3.2 * (double)sk_tiles / (double)G;
         if (cost < best - 1e-9) {
@@ -1650,8 +1754,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
         // valid sub-rows: 64x32 units (x 4 strips per tile column) or 16x128 units
         const int ms = s == 8 ? (rem_m + 63) / 64 : (rem_m + 15) / 16;
         const long long nonempty = re * per_tile(s) + (long long)tiles_n * ms * (s == 8 ? 4 : 1);
-        const double cost =
-            (qe > 0 ? qe * unit_us(1) + SECOND_LAUNCH_US : 0.0) + rounds(nonempty) * unit_us(s);
+        const double cost = (qe > 0 ? launch_us(1) + qe * round_us(1) + TAIL_LAUNCH_US : launch_us(s, rounds(nonempty))) +
+                            rounds(nonempty) * round_us(s);
         if (cost < best - 1e-9) {
           best = cost;
           split = s;
@@ -1664,8 +1768,8 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       }
     }
     if (allow_ksplit && ks_ok) {
-      const double slab_us = 1.02 * (unit_us(1) - unit_b(1)) / (double)ks_KT;
-      const double cost = (double)((tiles * ks_KT + G - 1) / G) * slab_us + 3 * unit_b(1) + 8.0 +
+      const double slab_us = 1.02 * sk_work_us(1) / (double)ks_KT;
+      const double cost = (double)((tiles * ks_KT + G - 1) / G) * slab_us + 3 * 2.8 + 8.0 +
                           MYD_KSPLIT_FIXUP_US * ((double)G / (double)tiles);
       if (cost < best - 1e-9) {
         best = cost;
