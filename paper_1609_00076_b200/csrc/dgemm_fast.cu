@@ -1530,11 +1530,14 @@ int set_max_ctas(int n) { return g_max_ctas.exchange(n); }
 // as units.  Ragged last tile column (N mod 128 in 1..64, e.g. cfg3a's
 // n = 4099): the column may be kept out of the full-tile raster and run in
 // the tail launch as units, only those covering valid columns scheduled.
-// Each candidate is costed with the per-unit time measured on the B200
-// (tools/plan_probe.py, profiles/plan_probe_r01.log): a unit of s-th of a
-// tile at depth K takes ideal/e_s + b_s microseconds on one SM (ideal at
-// 128 flop/clk, 1.965 GHz), and a second launch costs ~15 us; the cheapest
-// wins.  A ragged last tile row (M mod 128 in 1..64, and problems of <= 64
+// Each candidate is costed with whole-call times measured on the B200
+// (round 2: tools/unit_model_probe.py, profiles/r02/unit_model_r02a.log): a
+// launch of r rounds of 1/s-tile units at depth K takes launch_us(s) +
+// r * round_us(s) microseconds (round_us = ideal / e_s + c_s, ideal at
+// 128 flop/clk, 1.965 GHz), a tail launch after whole-tile rounds ~16 us, the
+// stream-K schedules their own fitted slab factors and fixed costs; the
+// cheapest wins (mean regret against the best forced plan ~1.1 % over seeded
+// random shapes, tools/planner_regret.py).  A ragged last tile row (M mod 128 in 1..64, and problems of <= 64
 // rows) gets the same treatment as a ragged column, with 64x32 or 16x128
 // units.  force_split pins the plan (tests and the tuner): 0 = heuristic,
 // 1 = full tiles only, 2 / 4 / 8 / 16 = every tile as 128x64 / 128x32 /
