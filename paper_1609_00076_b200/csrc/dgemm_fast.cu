@@ -137,7 +137,7 @@ __device__ unsigned long long g_fast_prof[8];
 #define MYD_KSPLIT_FIXUP_US 2.5  // K-split plan: owner's fix-up cost per piece of a tile (us, planner model)
 #endif
 #ifndef MYD_EDGE_BULK
-#define MYD_EDGE_BULK 1  // ragged problems of up to MYD_EDGE_BULK_WAVES waves of tiles run the EDGE instantiations:
+#define MYD_EDGE_BULK 1  // ragged problems of up to MYD_EDGE_BULK_WAVES waves of tiles (any size for K >= 1024) run the EDGE instantiations:
                          // partial units staged by bulk copies of their valid part (0: zero-filling LDGSTS everywhere)
 #endif
 #ifndef MYD_EDGE_BULK_WAVES
@@ -1242,10 +1242,13 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
   // depend on the plan or on which kernel a shard's tile lands in.
   const bool rk = MYD_SKIP_ZERO_KSTEPS && K % BK != 0 && BK - K % BK >= 4;
   // partial units worth their own instantiation (see the EDGE staging path)
+  // (long-K problems of more waves too: +0.5 % at 4093 x 4099 x 2047 and 5000^2 x 1000, while
+  // 6001^2 x 512 loses 0.3 % to the heavier producers, profiles/r02/ab_libs_r02f.log)
   [[maybe_unused]] const bool edge_bulk =
       (M % BM != 0 || N % BN != 0) &&
-      (long long)((M + fast::TILE_M - 1) / fast::TILE_M) * ((N + fast::TILE_N - 1) / fast::TILE_N) <=
-          (long long)MYD_EDGE_BULK_WAVES * sm_count();
+      (K >= 1024 ||
+       (long long)((M + fast::TILE_M - 1) / fast::TILE_M) * ((N + fast::TILE_N - 1) / fast::TILE_N) <=
+           (long long)MYD_EDGE_BULK_WAVES * sm_count());
 #define MYD_LAUNCH(CGT_, RK_)                                                                                   \
   do {                                                                                                            \
     if constexpr (VEC == 2 && BM != 16 && MYD_EDGE_BULK) {                                                        \
