@@ -840,6 +840,39 @@ def test_cuda_graph_capture_and_replay(torch_cuda, m, n, k):
     assert torch.equal(graphed, eager)
 
 
+@pytest.mark.timeout(300)
+def test_stream_k_workspace_is_per_stream(torch_cuda):
+    """Stream-K calls keep their partials and flags in a block owned by the
+    call's stream (up to 8 streams per device; further streams take a pooled
+    block with zeroed flags).  Ten streams issue interleaved stream-K calls
+    (1280^3: stream-K over units; 1792 x 1664 x 512: full-tile stream-K) on
+    their own C at the same time, twice over: every result is bitwise the
+    single-stream one, so no call ever saw another stream's partials or a
+    stale flag."""
+    torch = torch_cuda
+    shapes = [(1280, 1280, 1280), (1792, 1664, 512)]
+    ops, want = [], []
+    for (m, n, k) in shapes:
+        a, b, c, _ = dev_operands(torch, m, n, k)
+        w = c.clone()
+        run_dev(torch, m, n, k, a, m, b, k, w, m)
+        run_dev(torch, m, n, k, a, m, b, k, w, m)
+        ops.append((m, n, k, a, b, c))
+        want.append(w)
+    streams = [torch.cuda.Stream() for _ in range(10)]
+    outs = [[c.clone() for (_, _, _, _, _, c) in ops] for _ in streams]
+    torch.cuda.synchronize()
+    for rep in range(2):
+        for si, st in enumerate(streams):
+            for oi, (m, n, k, a, b, _) in enumerate(ops):
+                engine.dgemm_device(m, n, k, a.data_ptr(), m, b.data_ptr(), k, outs[si][oi].data_ptr(), m,
+                                    st.cuda_stream)
+    torch.cuda.synchronize()
+    for si in range(len(streams)):
+        for oi in range(len(ops)):
+            assert torch.equal(outs[si][oi], want[oi]), (si, oi)
+
+
 def test_more_than_2_31_elements_of_c(torch_cuda):
     """C with 2.15e9 elements (> 2^31: every index is 64-bit): fast path vs the
     exact kernel over the whole matrix within the headline bound, and the last
