@@ -1251,7 +1251,7 @@ cudaError_t launch_one(const Epilogue &ep, unsigned units, int M, int N, int K, 
            (long long)MYD_EDGE_BULK_WAVES * sm_count());
 #define MYD_LAUNCH(CGT_, RK_)                                                                                   \
   do {                                                                                                            \
-    if constexpr (VEC == 2 && BM != 16 && MYD_EDGE_BULK) {                                                        \
+    if constexpr (VEC == 2 && BM != 16 && MYD_EDGE_BULK && !SUM) {                                                \
       if (edge_bulk)                                                                                              \
         return launch_kernel<VEC, BM, BN, BK, SKM, CGT_, RK_, false, SUM, true>(                                  \
             ep, units, M, N, K, A, lda, B, ldb, C, ldc, tiles_m, tiles_n, tile0, edge, after_main, st, sk);       \
