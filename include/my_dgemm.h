@@ -233,6 +233,19 @@ MY_DGEMM_API int my_dgemm_tune(int m, int n, int k, int lda, int ldb, int ldc, i
  * (pkg/src/gemmforge/bench.py:238-311).  Returns 0, or -1 for an unknown plan.
  */
 MY_DGEMM_API int my_dgemm_plan_geometry(int plan, int k, int vec2, int *bm, int *bn, int *bk, int *stages);
+/*
+ * The tiled path's launch plan for a shape, as one line of text ("... units |
+ * stream-K | K-split | small split=.. sk_split=.. sk_dp_rounds=.. q=.. edge=..
+ * small=.. model_us=.."), without launching anything: the planner is host code
+ * (csrc/dgemm_fast.cu:launch_dgemm_fast), so this works without a GPU (it then
+ * plans for 148 SMs).  plan: 0 = the heuristic, what a default call of this
+ * shape runs (pins of my_dgemm_tune_set aside); -1 = the heuristic kept to the
+ * plan-invariant plans; otherwise a plan id as my_dgemm_tune reports them.
+ * The analogue of the reference's make_plan (pkg/src/gemmforge/parallel.py:60-105):
+ * the work decomposition as data, testable on its own.  Returns 0, -1 for bad
+ * arguments, -2 if the shape cannot be planned.
+ */
+MY_DGEMM_API int my_dgemm_plan_describe(int m, int n, int k, int lda, int ldb, int ldc, int plan, char *buf, int len);
 /* Pin `plan` for later calls of this shape and operand alignment (what
  * my_dgemm_tune records; engine.tune_grid's winner).  Negative status for a
  * bad argument or an unknown plan. */

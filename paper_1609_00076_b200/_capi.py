@@ -73,6 +73,7 @@ SIGNATURES = {
     "my_dgemm_plan_geometry": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),
                                     ctypes.POINTER(_I)]),
     "my_dgemm_tune_set": (_I, [_I, _I, _I, _I, _I, _I]),
+    "my_dgemm_plan_describe": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.c_char_p, _I]),
     "my_dgemm_set_max_ctas": (_I, [_I]),
     "my_dgemm_path": (_I, [_I, _I, ctypes.c_uint]),
     "my_dgemm_ipc_export": (_I, [_P, ctypes.c_char_p, ctypes.POINTER(_U64)]),

@@ -42,6 +42,7 @@
 #include <cstdlib>
 #include <atomic>
 #include <mutex>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -1550,6 +1551,8 @@ int small_variants();
 cudaError_t launch_dgemm_small(int variant, int M, int N, int K, const double *A, int64_t lda, const double *B,
                                int64_t ldb, double *C, int64_t ldc, cudaStream_t st, const Epilogue &ep, bool vec2);
 
+thread_local std::string *t_plan_out = nullptr;  // my_dgemm_plan_describe's dry run
+
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
                               const Epilogue &ep) {
@@ -1815,13 +1818,22 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
     const char *v = getenv("MY_DGEMM_PLAN_TRACE");
     return v && *v && *v != '0';
   }();
-  if (trace)
-    fprintf(stderr,
-            "my_dgemm plan: m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d sk_dp_rounds=%lld q=%lld raster=%dx%d "
-            "edge=%d small=%d\n",
-            M, N, K, (long long)tiles_m, tiles_n,
-            small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, sk_dp_rounds, q,
-            raster_m, raster_n, edge, small_v);
+  if (trace || t_plan_out) {
+    // (a full-tile stream-K call: the whole-tile rounds it will actually run)
+    const long long dp_shown = streamk && sk_split == 1 ? sk_dp_rounds : 0;
+    char line[320];
+    snprintf(line, sizeof line,
+             "m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d sk_dp_rounds=%lld q=%lld raster=%dx%d edge=%d small=%d "
+             "model_us=%.1f",
+             M, N, K, (long long)tiles_m, tiles_n,
+             small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, dp_shown, q,
+             raster_m, raster_n, edge, small_v, plan_best < 1e299 ? plan_best : -1.0);
+    if (trace && !t_plan_out) fprintf(stderr, "my_dgemm plan: %s\n", line);
+    if (t_plan_out) {  // my_dgemm_plan_describe: the plan only, nothing is launched
+      *t_plan_out = line;
+      return cudaSuccess;
+    }
+  }
   if (small_v > 0) return launch_dgemm_small(small_v, M, N, K, A, lda, B, ldb, C, ldc, stream, ep, vec2);
   if (ksplit) {
     SkWorkspace ws;
@@ -1939,6 +1951,24 @@ extern "C" __attribute__((visibility("default"))) int my_dgemm_plan_geometry(int
   if (bn) *bn = b;
   if (bk) *bk = c;
   if (stages) *stages = d;
+  return 0;
+}
+
+// The tiled path's launch plan for a shape, as text, without launching anything
+// (no GPU needed: the planner is host code; without a device it plans for 148
+// SMs).  plan: 0 the heuristic (what a default call runs, tuned plans aside),
+// -1 the heuristic kept to plan-invariant plans, else a pinned plan id.
+extern "C" __attribute__((visibility("default"))) int my_dgemm_plan_describe(int m, int n, int k, int lda, int ldb,
+                                                                             int ldc, int plan, char *buf, int len) {
+  if (m < 1 || n < 1 || k < 1 || lda < m || ldb < k || ldc < m || !buf || len < 1) return -1;
+  std::string out;
+  myd::t_plan_out = &out;
+  const cudaError_t e = myd::launch_dgemm_fast(m, n, k, nullptr, lda, nullptr, ldb, nullptr, ldc, nullptr, false, plan,
+                                               myd::Epilogue{});
+  myd::t_plan_out = nullptr;
+  cudaGetLastError();
+  if (e != cudaSuccess) return -2;
+  snprintf(buf, (size_t)len, "%s", out.c_str());
   return 0;
 }
 

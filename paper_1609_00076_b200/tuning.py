@@ -77,6 +77,34 @@ def plan_geometry(plan: int, k: int, vec2: bool = True) -> TilePoint | None:
     return TilePoint(v[0].value, v[1].value, v[2].value, v[3].value, plan)
 
 
+def describe_plan(m: int, n: int, k: int, lda: int | None = None, ldb: int | None = None, ldc: int | None = None,
+                  plan: int = 0) -> dict:
+    """The tiled path's launch plan for a shape, from the planner itself
+    (my_dgemm_plan_describe: host code, nothing is launched, no GPU needed --
+    without a device it plans for 148 SMs).  The reference's make_plan
+    (pkg/src/gemmforge/parallel.py:60-105) as data: `kind` is "units",
+    "stream-K", "K-split" or "small"; `split` / `sk_split` the units per tile
+    (1 = full 128x128 tiles), `sk_dp_rounds` the whole-tile rounds ahead of a
+    full-tile stream-K phase, `q` the whole-tile rounds (or tiles) of the main
+    launch, `edge` the edge plan, `small` the small-block variant, `model_us`
+    the planner's cost of its persistent-kernel choice.  plan: 0 the heuristic,
+    -1 the heuristic kept to plan-invariant plans, else a pinned plan id."""
+    lib = _capi.load()
+    buf = ctypes.create_string_buffer(512)
+    st = lib.my_dgemm_plan_describe(m, n, k, lda or m, ldb or k, ldc or m, plan, buf, len(buf))
+    if st != 0:
+        raise ValueError(f"my_dgemm_plan_describe({m}, {n}, {k}) failed with status {st}")
+    text = buf.value.decode()
+    out: dict = {"text": text}
+    for tok in text.split():
+        if "=" in tok:
+            key, val = tok.split("=", 1)
+            out[key] = float(val) if key == "model_us" else (val if "x" in val else int(val))
+        else:
+            out["kind"] = tok
+    return out
+
+
 def compiled_points(k: int, vec2: bool = True) -> list[TilePoint]:
     """Every launch plan's blocking parameters at depth k (one point per plan;
     stream-K plans share their unit shape's geometry)."""

@@ -296,3 +296,59 @@ def test_tile_grid_expansion_and_tie_break(lib):
     assert tuning._beats(10.0, b, 10.0, a)  # smaller footprint wins the tie
     assert not tuning._beats(10.0, a, 10.0, b)
     assert tuning._beats(10.5, a, 10.0, b)
+
+
+# ------------------------------------------------------------------ the planner, as data (no GPU)
+
+def test_planner_picks_the_measured_plans_for_the_baseline_shapes(lib):
+    """my_dgemm_plan_describe runs the planner (host code) without launching:
+    the picks the B200 measurements back (DESIGN 4c, profiles/r02/) are pinned
+    here so a change to the cost model that flips one is seen on CPU.  The
+    reference's make_plan (parallel.py:60-105) is likewise tested as data."""
+    from paper_1609_00076_b200 import tuning
+
+    d = tuning.describe_plan
+    # cfg4 (16384^2 x 256): whole-tile rounds -- every tile in the stream-K phase measured 4.05 ms vs 3.93
+    p = d(16384, 16384, 256)
+    assert p["kind"] == "units" and p["split"] == 1 or (p["kind"] == "stream-K" and p["sk_dp_rounds"] >= 100)
+    # cfg5 and cfg2@8192: whole-tile rounds, the last one to two waves as a stream-K tail
+    p = d(32768, 32768, 32768)
+    assert p["kind"] == "stream-K" and p["sk_split"] == 1 and p["sk_dp_rounds"] == 32768 // 128 * (32768 // 128) // 148 - 1
+    p = d(8192, 8192, 8192)
+    assert p["kind"] == "stream-K" and p["sk_split"] == 1 and p["sk_dp_rounds"] == 26
+    assert abs(p["model_us"] / 30050.0 - 1.0) < 0.02  # the model's absolute level (measured 30.0-30.1 ms)
+    # below one wave: stream-K over 128x32 units at 1024^3 (72.7 us vs 77.1 as 128x64 units)
+    p = d(1024, 1024, 1024)
+    assert (p["kind"], p["sk_split"]) == ("stream-K", 4) and abs(p["model_us"] / 72.0 - 1.0) < 0.05
+    # 2.2 waves, long K: every tile in the stream-K phase (696 us vs 715 after a whole-tile round)
+    p = d(2304, 2304, 2304)
+    assert (p["kind"], p["sk_split"], p["sk_dp_rounds"]) == ("stream-K", 1, 0)
+    # several waves at K = 128: 128x64 units (78.3 us), not full tiles (93.8 us)
+    p = d(5376, 1536, 128)
+    assert (p["kind"], p["split"]) == ("units", 2)
+    # cfg1: one round of 64x32 units; the sub-wave cfg2 point and cfg3d: the small-block kernel
+    p = d(512, 512, 512)
+    assert (p["kind"], p["split"]) == ("units", 8)
+    assert d(256, 256, 256)["kind"] == "small" and d(37, 53, 71, 44, 76, 40)["kind"] == "small"
+    # cfg3a: whole-tile rounds with the ragged last tile column run as strips in the tail launch
+    p = d(4093, 4099, 2047, 4100, 2052, 4096)
+    assert p["kind"] == "units" and p["edge"] >= 1 and p["q"] == 6
+
+
+def test_planner_never_picks_the_k_split_plan_unasked(lib):
+    """The K-split plan is the one plan that is not plan-invariant: the
+    heuristic (plan 0) must never choose it unless MY_DGEMM_KSPLIT=1, the
+    plan-invariant heuristic (-1, what shards run) is the same choice, and
+    pinning it (48) works only where the shape allows."""
+    from paper_1609_00076_b200 import tuning
+
+    assert os.environ.get("MY_DGEMM_KSPLIT", "0") in ("", "0")
+    for s in range(256, 4097, 128):
+        for (m, n, k) in ((s, s, s), (s, 2 * s, 640), (s + 5, s, 2047)):
+            a, b = tuning.describe_plan(m, n, k), tuning.describe_plan(m, n, k, plan=-1)
+            assert a["kind"] != "K-split" and a["text"] == b["text"], (m, n, k)
+    assert tuning.describe_plan(1024, 1024, 1024, plan=48)["kind"] == "K-split"
+    assert tuning.describe_plan(8192, 8192, 8192, plan=48)["kind"] != "K-split"  # more tiles than SMs
+    assert tuning.describe_plan(768, 640, 96, plan=48)["kind"] != "K-split"      # fewer than two slabs per CTA
+    with pytest.raises(ValueError):
+        tuning.describe_plan(0, 4, 4)
