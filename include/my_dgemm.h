@@ -217,7 +217,8 @@ MY_DGEMM_API int my_dgemm_diff_report(int64_t m, int64_t n, const double *X, int
  * kernel for this shape (heuristic, full tiles only, all 128x64 / 128x32 /
  * 64x32 units) on scratch device operands and remembers the fastest for
  * later calls of the same shape and operand alignment in this process.
- * Plans are bitwise-equivalent: tuning changes speed, never results.
+ * These plans are bitwise-equivalent: tuning changes speed, never results
+ * (the opt-in K-split plan, 48, is not among them).
  * out_plan: 0 heuristic, 1 full tiles, 2/4/8 units per tile (128x64 / 128x32 /
  * 64x32), 16 for 16x128 units, 32 / 34 / 36 / 40 stream-K over full tiles /
  * 128x64 / 128x32 / 64x32 units.

@@ -36,7 +36,9 @@
 // starting at C) does not depend on the unit shape, the tile position, the
 // K-slab depth, the launch plan or which CTA runs which slabs, so every plan
 // (stream-K included) and every k-chunking at multiples of 16 gives bitwise
-// the same C, down to the sign of zeros.
+// the same C, down to the sign of zeros.  (One exception, never chosen unless
+// asked for: the K-split plan, which sums partial chains -- see the SUM
+// instantiation and include/my_dgemm.h, MY_DGEMM_PLAN_INVARIANT.)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -1545,7 +1547,9 @@ int set_max_ctas(int n) { return g_max_ctas.exchange(n); }
 // rows) gets the same treatment as a ragged column, with 64x32 or 16x128
 // units.  force_split pins the plan (tests and the tuner): 0 = heuristic,
 // 1 = full tiles only, 2 / 4 / 8 / 16 = every tile as 128x64 / 128x32 /
-// 64x32 / 16x128 units.  Every plan computes bitwise the same C.
+// 64x32 / 16x128 units, 32 + s = stream-K over those, 64 + v = the small-block
+// kernel.  Every one of these computes bitwise the same C; 48, the opt-in
+// K-split plan, is the exception (deterministic, within the tolerance).
 double small_cost_us(int v, int M, int N, int K, int G);  // dgemm_small.cu
 int small_variants();
 cudaError_t launch_dgemm_small(int variant, int M, int N, int K, const double *A, int64_t lda, const double *B,
