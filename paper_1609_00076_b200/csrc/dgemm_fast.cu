@@ -146,6 +146,14 @@ __device__ unsigned long long g_fast_prof[8];
 #ifndef MYD_EDGE_BULK_WAVES
 #define MYD_EDGE_BULK_WAVES 4
 #endif
+#ifndef MYD_SKIP_FIRST_C_PREFETCH
+#define MYD_SKIP_FIRST_C_PREFETCH 1  // 0: L2-prefetch the first unit's C block too (A/B timing)
+#endif
+#if MYD_SKIP_FIRST_C_PREFETCH
+#define MYD_FIRST_C_PREFETCH_OK(first) (!(first))
+#else
+#define MYD_FIRST_C_PREFETCH_OK(first) true
+#endif
 #ifndef MYD_EP_SHFL
 #define MYD_EP_SHFL 1  // 128-byte-per-column epilogue stores (lane-pair swap); 0 = plain fragment stores
 #endif
@@ -498,7 +506,11 @@ __global__ void __launch_bounds__(fast::THREADS, 1)
       // the BLAS epilogue reads C at the end instead).  The copies are issued
       // while the consumers finish the previous unit, so the C load is off the
       // critical path and spread in time instead of bursting at unit start.
-      if (CG && (!ep.blas || ep.beta != 0.0) && sg.from_c) {  // BLAS: C is read by the epilogue
+      // (not for a launch's first unit: the consumers read that C block at the
+      // same moment anyway, and the 128 prefetch operations queue in the
+      // bulk-copy engine ahead of the first slabs -- the first slab went out
+      // 2.8 us after the grid dependency cleared, profiles/r02/timeline_1536_r02a.log)
+      if (CG && (!ep.blas || ep.beta != 0.0) && sg.from_c && MYD_FIRST_C_PREFETCH_OK(first_seg)) {  // BLAS: C is read by the epilogue
         const int rows = max(0, min(BM, M - m0));
         const int col = pw * (BN / PRODUCER_WARPS) + lane;
         if (c_aligned && rows > 0 && rows % 2 == 0 && lane < BN / PRODUCER_WARPS && n0 + col < N)
