@@ -1568,6 +1568,14 @@ cudaError_t launch_dgemm_small(int variant, int M, int N, int K, const double *A
                                int64_t ldb, double *C, int64_t ldc, cudaStream_t st, const Epilogue &ep, bool vec2);
 
 thread_local std::string *t_plan_out = nullptr;  // my_dgemm_plan_describe's dry run
+bool plan_trace_env() {  // MY_DGEMM_PLAN_TRACE=1: print each call's launch plan to stderr
+  static const bool on = [] {
+    const char *v = getenv("MY_DGEMM_PLAN_TRACE");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+inline bool trace_wanted() { return t_plan_out != nullptr || plan_trace_env(); }
 
 cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda, const double *B, int64_t ldb,
                               double *C, int64_t ldc, cudaStream_t stream, bool force_vec1, int force_split,
@@ -1812,6 +1820,13 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
   // few long unit chains; bitwise the same C.  force_split 64 + v pins
   // variant v (64: the cheapest variant by the model).
   int small_v = 0;
+  double small_us = -1.0;  // the small-block kernel's cheapest variant by its model (trace / plan_describe)
+  if (trace_wanted() && force_split == 0 && !force_ksplit) {
+    for (int v = 1; v <= small_variants(); ++v) {
+      const double c = small_cost_us(v, M, N, K, (int)G);
+      if (small_us < 0 || c < small_us) small_us = c;
+    }
+  }
   if (force_split >= 64) {
     small_v = force_split - 64;
     if (small_v == 0) {
@@ -1830,20 +1845,17 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       if (c < sbest - 1e-9) sbest = c, small_v = v;
     }
   }
-  static const bool trace = [] {  // MY_DGEMM_PLAN_TRACE=1: print each call's launch plan to stderr
-    const char *v = getenv("MY_DGEMM_PLAN_TRACE");
-    return v && *v && *v != '0';
-  }();
+  const bool trace = plan_trace_env();
   if (trace || t_plan_out) {
     // (a full-tile stream-K call: the whole-tile rounds it will actually run)
     const long long dp_shown = streamk && sk_split == 1 ? sk_dp_rounds : 0;
     char line[320];
     snprintf(line, sizeof line,
              "m=%d n=%d k=%d tiles=%lldx%d %s split=%d sk_split=%d sk_dp_rounds=%lld q=%lld raster=%dx%d edge=%d small=%d "
-             "model_us=%.1f",
+             "model_us=%.1f small_us=%.1f",
              M, N, K, (long long)tiles_m, tiles_n,
              small_v ? "small" : (ksplit ? "K-split" : (streamk ? "stream-K" : "units")), split, sk_split, dp_shown, q,
-             raster_m, raster_n, edge, small_v, plan_best < 1e299 ? plan_best : -1.0);
+             raster_m, raster_n, edge, small_v, plan_best < 1e299 ? plan_best : -1.0, small_us);
     if (trace && !t_plan_out) fprintf(stderr, "my_dgemm plan: %s\n", line);
     if (t_plan_out) {  // my_dgemm_plan_describe: the plan only, nothing is launched
       *t_plan_out = line;

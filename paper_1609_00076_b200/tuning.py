@@ -87,7 +87,9 @@ def describe_plan(m: int, n: int, k: int, lda: int | None = None, ldb: int | Non
     (1 = full 128x128 tiles), `sk_dp_rounds` the whole-tile rounds ahead of a
     full-tile stream-K phase, `q` the whole-tile rounds (or tiles) of the main
     launch, `edge` the edge plan, `small` the small-block variant, `model_us`
-    the planner's cost of its persistent-kernel choice.  plan: 0 the heuristic,
+    the planner's cost of its persistent-kernel choice, `small_us` the
+    small-block kernel's cheapest variant by its own model (-1 when not
+    evaluated).  plan: 0 the heuristic,
     -1 the heuristic kept to plan-invariant plans, else a pinned plan id."""
     lib = _capi.load()
     buf = ctypes.create_string_buffer(512)
@@ -99,7 +101,7 @@ def describe_plan(m: int, n: int, k: int, lda: int | None = None, ldb: int | Non
     for tok in text.split():
         if "=" in tok:
             key, val = tok.split("=", 1)
-            out[key] = float(val) if key == "model_us" else (val if "x" in val else int(val))
+            out[key] = float(val) if key.endswith("_us") else (val if "x" in val else int(val))
         else:
             out["kind"] = tok
     return out
