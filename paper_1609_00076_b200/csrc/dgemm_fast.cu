@@ -1336,8 +1336,8 @@ std::atomic<unsigned long long> g_sk_epochs{0};
 
 // Workspace of one stream-K / K-split call: one partial unit per CTA plus
 // per-warp flags.  Normally a block owned by the call's stream (up to
-// SK_STREAMS streams per device, keyed by cudaStreamGetId, allocated and its
-// flags zeroed once, never freed): calls on one stream run in order -- a PDL
+// SK_STREAMS streams per device, keyed by cudaStreamGetId, allocated from the
+// stream-ordered pool and its flags zeroed on that stream once, never freed): calls on one stream run in order -- a PDL
 // successor touches global memory only after its griddepcontrol.wait, i.e.
 // after the previous grid has completed -- and every launch has its own epoch,
 // so flags left by earlier calls never match and nothing has to be zeroed or
@@ -1395,11 +1395,13 @@ struct SkWorkspace {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t ctas = (size_t)std::max(G, sms);
+    // (stream-ordered allocation and zeroing on the owning stream itself, once: unlike cudaMalloc /
+    // cudaMemset they do not disturb a stream capture another thread may have open)
     void *b = nullptr;
-    if (cudaMalloc(&b, part_bytes(ctas) + flag_bytes(ctas)) != cudaSuccess ||
-        cudaMemset(static_cast<char *>(b) + part_bytes(ctas), 0, flag_bytes(ctas)) != cudaSuccess) {
+    if (cudaMallocAsync(&b, part_bytes(ctas) + flag_bytes(ctas), st) != cudaSuccess ||
+        cudaMemsetAsync(static_cast<char *>(b) + part_bytes(ctas), 0, flag_bytes(ctas), st) != cudaSuccess) {
       cudaGetLastError();
-      if (b) cudaFree(b);
+      if (b) cudaFreeAsync(b, st);
       return false;
     }
     d.own[d.n++] = SkOwned{id, b, ctas};
