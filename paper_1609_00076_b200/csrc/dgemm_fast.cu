@@ -1743,9 +1743,10 @@ cudaError_t launch_dgemm_fast(int M, int N, int K, const double *A, int64_t lda,
       if (ragged_mn && (M < TILE_M || N < TILE_N)) continue;  // (narrower than a tile: the edge plans)
       const double f = s == 2 ? 1.037 : (s == 4 ? 1.058 : 1.086), fixed = s == 2 ? 12.0 : (s == 4 ? 10.3 : 9.9);
       const double slab_us = f * sk_work_us(s) / (double)KT;
-      // (the fit covers 1.3 - 2.9 units per CTA; each further unit boundary ~3 us)
+      // (the fit covers 1.3 - 2.9 units per CTA; each further unit boundary ~2 us:
+      // 2688 x 4096 x 512 as 128x64 units 345.8 us, 2304^3 709.5 us)
       const double cost = (double)((units_s * KT + G - 1) / G) * slab_us + fixed +
-                          3.0 * std::max(0.0, (double)units_s / (double)G - 2.0);
+                          2.0 * std::max(0.0, (double)units_s / (double)G - 2.0);
       if (cost < best - 1e-9) {
         best = cost;
         streamk = true;
