@@ -12,16 +12,20 @@
 //                         (launch_dgemm_fast); a partial last wave can run
 //                         as stream-K (slabs of cut tiles split between two
 //                         CTAs, the exact accumulator state handed over, so C
-//                         is unchanged); launches overlap their neighbours by
-//                         programmatic dependent launch;
+//                         is unchanged; its workspace is owned by the stream,
+//                         nothing is allocated or zeroed per call); launches
+//                         overlap their neighbours by programmatic dependent
+//                         launch;
 //   loop 4 (pc)        -> the in-CTA K loop over BK-deep slabs;
 //   pack_a / pack_b    -> producer warps stage each A and B slab (and, for
 //                         narrow units, first the unit's C block; full tiles
 //                         read C from global, prefetched to L2) into a
 //                         multi-stage shared-memory ring: bulk copies by the
 //                         TMA engine (cp.async.bulk) for aligned interior
-//                         data, zero-filling cp.async (LDGSTS) at the edges
-//                         and for 16x128 units; no pack pass touches HBM;
+//                         data (partial units of small or long-K ragged
+//                         problems too: the valid part only, EDGE), else
+//                         zero-filling cp.async (LDGSTS) -- a ragged last K
+//                         slab, 16x128 units; no pack pass touches HBM;
 //   loops 2/1 + _mk    -> 8 consumer warps, each a register tile of C built
 //                         from DMMA.8x8x4 fragments (mma.sync f64).  FP64 has
 //                         no tcgen05 kind on sm_100a; the DMMA pipe measured
